@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark of the GridMaker hot path (fwd + bwd) on B200.
+
+Metric (BASELINE.json): grids/s for forward + backward at 0.5 A / 48^3 /
+28 channels / batch 50 (config C2: receptor pocket ~1000 atoms + 30-atom
+ligand, synthetic per SURVEY 8(d)), with the fused random rotation +
+translation augmentation, plus HBM GB/s vs roofline.
+
+One step = one pass of the hot path over one batch of 50 examples per GPU:
+prepare (transform + boxes) -> forward (every voxel written) -> backward
+(coordinate gradients of every atom).
+
+* value: inputs resident in HBM (packed once), grid_grad ~ N(0,1) resident.
+* e2e: through the public API with host inputs: each step copies the packed
+  atoms host->device from pinned memory, grids, back-propagates the loss
+  1/2 |grid|^2 (grid_grad = grid, stays on the device as a CNN's would) and
+  reads the coordinate gradients back device->host.
+* N > 1 (torchrun): every rank grids its own 50 examples (weak scaling, no
+  collective on the path); time = max over ranks of the device time.
+
+``--impl reference`` times the CPU oracle (C restatement of the reference's
+numba kernels, OpenMP over all host cores) on a bounded sample instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (resolution, dimension, binary, vector, seed, batch per GPU, aug)
+    "c2": dict(resolution=0.5, dimension=23.5, binary=False, vector=False, seed=2, batch=50,
+               workload="C2: receptor pocket 1000 atoms + ligand 30 atoms, 28 ch, 48^3, "
+                        "batch 50/GPU, fwd+bwd, random rotation + 2 A translation"),
+    "c3": dict(resolution=0.5, dimension=23.5, binary=True, vector=False, seed=2, batch=50,
+               workload="C3: C2 batch, binary occupancy, random rotation + 2 A translation"),
+    "c4": dict(resolution=0.5, dimension=23.5, binary=False, vector=True, seed=4, batch=50,
+               workload="C4: C2 shapes, vector types (25% dense weights), fwd+bwd with type grads"),
+    "c5": dict(resolution=0.25, dimension=23.75, binary=False, vector=False, seed=2, batch=50,
+               workload="C5: 0.25 A / 96^3, 28 ch, 50 examples per GPU (400 over 8 GPUs)"),
+}
+
+
+def load_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_batch(cfg, rank, n=None):
+    from paper_1912_04822_b200 import synthetic
+
+    n = cfg["batch"] if n is None else n
+    # rank r grids examples [r*B, (r+1)*B) of one global stream
+    rng = np.random.default_rng(cfg["seed"])
+    exs = []
+    for i in range((rank + 1) * n):
+        ex = synthetic.complex_example(rng, vector=cfg["vector"])
+        if i >= rank * n:
+            exs.append(ex)
+    return exs
+
+
+def bytes_model(cfg, exs, footprint):
+    """Algorithmic bytes per grid."""
+    D = int(np.floor(cfg["dimension"] / cfg["resolution"] + 0.5)) + 1
+    C = sum(cs.num_types for cs in exs[0].coord_sets)
+    A = np.mean([sum(cs.num_atoms for cs in ex.coord_sets) for ex in exs])
+    T = 14
+    b_in = (16 + 4 * T) if cfg["vector"] else 20
+    b_out = 12 + (4 * T if cfg["vector"] else 0)
+    fwd = 4 * C * D ** 3 + A * b_in + 144
+    if cfg["binary"]:
+        bwd = A * b_out
+    else:
+        bwd = 4 * footprint + A * b_in + 144 + A * b_out
+    return float(fwd), float(bwd), D, C
+
+
+def cpu_oracle_rate(cfg, exs, budget_s=12.0, threads=None):
+    """Oracle fwd+bwd grids/s on this host's cores over a bounded sample."""
+    import oracle
+
+    oracle.build()
+    n0 = oracle.num_threads()
+    cores = threads or len(os.sched_getaffinity(0))
+    oracle.set_num_threads(cores)
+    go = oracle.GridOracle(resolution=cfg["resolution"], dimension=cfg["dimension"],
+                           binary=cfg["binary"])
+    sample = exs[:8]
+
+    def one():
+        grid = go.forward_batch(sample, random_rotation=True, random_translation=2.0,
+                                rng=np.random.default_rng(0))
+        if not cfg["binary"]:
+            gg = grid  # gradient of 1/2 |grid|^2
+            go.backward_batch(sample, gg, random_rotation=True, random_translation=2.0,
+                              rng=np.random.default_rng(0))
+
+    one()  # warm (page-in)
+    times = []
+    t_all = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        one()
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > budget_s or len(times) >= 50:
+            break
+    oracle.set_num_threads(n0)
+    med = statistics.median(times)
+    return len(sample) / med, cores, len(times), med
+
+
+def run_reference(args, cfg):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    exs = make_batch(cfg, 0, n=8)
+    import oracle
+
+    oracle.build()
+    cores = len(os.sched_getaffinity(0))
+    oracle.set_num_threads(cores)
+    go = oracle.GridOracle(resolution=cfg["resolution"], dimension=cfg["dimension"],
+                           binary=cfg["binary"])
+
+    def step(seed):
+        grid = go.forward_batch(exs, random_rotation=True, random_translation=2.0,
+                                rng=np.random.default_rng(seed))
+        if not cfg["binary"]:
+            go.backward_batch(exs, grid, random_rotation=True, random_translation=2.0,
+                              rng=np.random.default_rng(seed))
+
+    for w in range(args.warmup):
+        step(w)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        step(1000 + k)
+    el = time.perf_counter() - t0
+    val = len(exs) * args.steps / el
+    line = {
+        "impl": "reference", "metric": "grids/sec (fwd+bwd, 48^3x28ch, batch 50)",
+        "value": val, "unit": "grids/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000 * el / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64 (oracle) -> f32 grids",
+        "data": "synthetic", "config": {"workload": cfg["workload"] + " (CPU sample: 8 examples/step)",
+                                        "batch_per_step": len(exs)},
+        "cpu_baseline": {"value": val, "unit": "grids/s", "cores": cores, "kind": "port",
+                         "sample": f"{len(exs)} examples fwd+bwd per step, OpenMP over sets/atoms"},
+        "e2e": {"value": val, "unit": "grids/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1912_04822_b200 import GridMaker, _native
+
+    exs = make_batch(cfg, rank)
+    gm = GridMaker(resolution=cfg["resolution"], dimension=cfg["dimension"],
+                   binary=cfg["binary"], device=dev)
+    D = gm.points_per_side()
+    pb = gm.pack(exs)
+    N, C = pb.nexamples, pb.nchannels
+    out = torch.empty((N, C, D, D, D), dtype=torch.float32, device=dev)
+    gg = torch.randn((N, C, D, D, D), generator=torch.Generator(device=dev).manual_seed(7),
+                     device=dev, dtype=torch.float32)
+    cg = torch.empty((pb.natoms, 3), dtype=torch.float32, device=dev)
+    tg = torch.empty((max(pb.nweights, 1),), dtype=torch.float32, device=dev) if pb.vector_mode else None
+    rng = np.random.default_rng(1234 + rank)
+    stream = torch.cuda.current_stream(dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(fwd_ev=None, bwd_ev=None):
+        # events bracket exactly the k_forward / k_backward launches
+        gm.forward_packed(pb, out, random_rotation=True, random_translation=2.0, rng=rng,
+                          events=fwd_ev)
+        gm.backward_packed(pb, gg, reuse_prepared=True, coord_grad=cg, type_grad=tg,
+                           events=bwd_ev)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+    footprint = int((out != 0).sum().item()) / N if not cfg["binary"] else 0
+    fwd_b, bwd_b, D, C = bytes_model(cfg, exs, footprint)
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    clocks = ClockSampler(local)
+    fevs = [(ev(), ev()) for _ in range(args.steps)]
+    bevs = [(ev(), ev()) for _ in range(args.steps)]
+    t_start, t_end = ev(), ev()
+    barrier()
+    _native.launch_count(reset=True)
+    clocks.start()
+    t_start.record(stream)
+    for k in range(args.steps):
+        step(fevs[k], bevs[k])
+    t_end.record(stream)
+    barrier()
+    clk = clocks.stop()
+    launches = _native.launch_count()
+    ms = t_start.elapsed_time(t_end) / args.steps
+    fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in fevs)
+    bwd_ms = statistics.mean(a.elapsed_time(b) for a, b in bevs)
+    if ws > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = ws * N / (ms / 1000.0)
+
+    # ---- e2e: public API with host inputs, D2H of the coordinate gradients ----
+    e2e = None
+    if not args.no_e2e:
+        host_cg = torch.empty((pb.natoms, 3), dtype=torch.float32, pin_memory=True)
+
+        def e2e_step():
+            pb.upload()  # H2D of the packed atoms (pinned)
+            gm.forward_packed(pb, out, random_rotation=True, random_translation=2.0, rng=rng)
+            gm.backward_packed(pb, out, reuse_prepared=True, coord_grad=cg, type_grad=tg)
+            host_cg.copy_(cg, non_blocking=True)
+
+        for _ in range(3):
+            e2e_step()
+        a, b = ev(), ev()
+        barrier()
+        a.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        b.record(stream)
+        barrier()
+        e_ms = a.elapsed_time(b) / args.steps
+        if ws > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": ws * N / (e_ms / 1000.0), "unit": "grids/s",
+               "h2d_bytes_per_step": pb.h2d_bytes + 8 * 18 * N,
+               "d2h_bytes_per_step": int(host_cg.numel() * 4),
+               "note": "GridMaker.forward_packed/backward_packed with a pinned host->device "
+                       "upload of the atoms each step, loss 1/2|grid|^2, coordinate "
+                       "gradients read back to host"}
+
+    peak, peak_src = load_peak()
+    achieved = fwd_b * N / (fwd_ms / 1000.0) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / f"traffic_{args.config}.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": "grids/sec (fwd+bwd, 48^3x28ch, batch 50)" if args.config == "c2"
+        else f"grids/sec (fwd+bwd, {args.config})",
+        "value": value, "unit": "grids/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 geometry where exactness needs it)",
+        "data": "synthetic",
+        "config": {"workload": cfg["workload"], "global_batch": ws * N, "batch_per_gpu": N,
+                   "grid": f"{C}x{D}^3", "parallelism": f"example-sharded x{ws}",
+                   "l2": "output 619 MB/step > 126 MB L2 (no flush needed)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel": "k_forward (prepare+forward launch pair)",
+                     "algorithmic_bytes_per_launch": fwd_b * N,
+                     "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
+                     "bwd_gbs": bwd_b * N / (bwd_ms / 1000.0) / 1e9,
+                     "step_gbs": (fwd_b + bwd_b) * N / (ms / 1000.0) / 1e9,
+                     "step_frac": (fwd_b + bwd_b) * N / (ms / 1000.0) / 1e9 / peak,
+                     "footprint_F_per_grid": footprint},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        rate, cores, reps, med = cpu_oracle_rate(cfg, exs, args.cpu_budget)
+        line["cpu_baseline"] = {"value": rate, "unit": "grids/s", "cores": cores, "kind": "port",
+                                "sample": f"8 examples of the same workload fwd+bwd, median of "
+                                          f"{reps} reps ({med * 1000:.0f} ms each), C oracle "
+                                          "with OpenMP"}
+    if rank == 0:
+        print(json.dumps(line))
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

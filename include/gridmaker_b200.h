@@ -1,0 +1,165 @@
+/*
+ * gridmaker_b200.h -- C ABI of the B200 GridMaker hot path.
+ *
+ * Drop-in boundary for the reference's kernel layer
+ * (/root/reference/pkg/src/voxmol/_kernels.py), which voxelizer.py calls with
+ * packed CSR arrays (voxelizer.py:372-435 forward, 293-300 backward).  Every
+ * entry point uses plain pointers and sizes; no C++ or torch types cross the
+ * boundary, nothing throws, and every function returns a gm_status (0 = OK,
+ * details from gm_last_error()).
+ *
+ * Two groups of entry points:
+ *
+ * 1. Reference-shaped kernels, same argument meaning as _kernels.py:
+ *      gm_forward_index_sets   <- _kernels.forward_index_sets  (_kernels.py:33-36)
+ *      gm_forward_vector_sets  <- _kernels.forward_vector_sets (_kernels.py:116-120)
+ *      gm_backward_index       <- _kernels.backward_index      (_kernels.py:209-210)
+ *      gm_backward_vector      <- _kernels.backward_vector     (_kernels.py:258-260)
+ *    The *_host variants take HOST (numpy) buffers exactly like the numba
+ *    kernels and do the host<->device copies internally (what a ctypes shim in
+ *    voxelizer.py binds).  The *_dev variants take device
+ *    pointers and a cudaStream_t (as void*).
+ *
+ * 2. The fused batch path used by the Python GridMaker (device pointers):
+ *      gm_workspace_bytes, gm_prepare (transform + localise + boxes),
+ *      gm_forward, gm_backward (batched over every set of every example).
+ *
+ * Layouts (C order): out / grid_grad (nexamples, nchannels, D, D, D) float32
+ * with k (z) contiguous, i.e. out[e][c][i][j][k] at voxel
+ * origin + res*(i, j, k) (_kernels.py:86-113).
+ */
+#ifndef GRIDMAKER_B200_H
+#define GRIDMAKER_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int gm_status;
+#define GM_OK 0
+#define GM_ERR_INVALID 1   /* bad argument (null pointer, size, mode) */
+#define GM_ERR_CUDA 2      /* CUDA launch / copy / allocation failure */
+
+/* Gridding parameters (GridMaker fields, voxelizer.py:97-105, plus derived). */
+typedef struct {
+    double resolution;               /* grid spacing (A) */
+    double dimension;                /* cube side (A) */
+    double radius_scale;             /* multiplies atom / type radii */
+    double gaussian_radius_multiple; /* grm */
+    double radius_multiple;          /* (1 + 2 grm^2) / (2 grm), voxelizer.py:148-152 */
+    int32_t npts;                    /* D = floor(dimension/resolution + 0.5) + 1 */
+    int32_t binary;                  /* 0/1 */
+    int32_t radius_type_indexed;     /* 0/1 (vector mode only) */
+    int32_t matmul_order_1;          /* FMA order of numpy (1,3)@(3,3), -1 = default */
+    int32_t matmul_order_n;          /* FMA order of numpy (N,3)@(3,3), N >= 2 */
+} gm_params;
+
+/* A packed batch in device memory (CSR over sets, like voxelizer._run_batch).
+ * Sets of one example are consecutive; atoms of one set are consecutive;
+ * items (see below) of one example are consecutive. */
+typedef struct {
+    int32_t nexamples, nsets, natoms, nitems, nchannels;
+    int32_t vector_mode;             /* 0: index types, 1: type_vector weights */
+    /* atoms */
+    const float *coords32;           /* (natoms,3) input frame, or NULL */
+    const double *coords64;          /* (natoms,3) input frame, or NULL */
+    const double *atom_radius;       /* (natoms) radius * radius_scale (f64) */
+    const int32_t *atom_set;         /* (natoms) packed set index */
+    const int32_t *atom_type;        /* (natoms) type index (index mode) */
+    /* sets */
+    const int32_t *set_start, *set_end, *set_example, *set_choff, *set_t; /* (nsets) */
+    const int32_t *set_wstart;       /* (nsets) offset of the set's weight rows (vector) */
+    const float *weights;            /* packed (atoms x T) rows per set (vector) */
+    int32_t nweights;                /* total packed weight / type-gradient entries */
+    const double *type_radius;       /* packed per set at set_trstart, scaled (vector) */
+    const int32_t *set_trstart;      /* (nsets) */
+    /* forward items: index mode -> one per atom (item_atom may be NULL = identity);
+     * vector mode -> one per nonzero weight, atom-major then channel. */
+    const int32_t *item_atom;        /* (nitems) or NULL */
+    const int32_t *item_channel;     /* (nitems) channel within the set, or NULL = atom_type */
+    const float *item_weight;        /* (nitems) or NULL = 1 */
+    const double *item_radius;       /* (nitems) scaled radius, or NULL = atom_radius */
+    const int32_t *ex_item_start, *ex_item_end; /* (nexamples) */
+    /* per example */
+    const double *origins;           /* (nexamples,3) center - dimension/2 */
+    const double *xforms;            /* (nexamples,15) R row-major, center, translation; NULL = none */
+} gm_batch;
+
+/* Device scratch needed by gm_prepare / gm_forward / gm_backward. */
+size_t gm_workspace_bytes(int32_t natoms, int32_t nitems);
+
+gm_status gm_prepare(const gm_params *p, const gm_batch *b, void *workspace,
+                     size_t workspace_bytes, void *stream);
+/* out: (nexamples, nchannels, D, D, D) f32 device; every voxel is written. */
+gm_status gm_forward(const gm_params *p, const gm_batch *b, const void *workspace,
+                     float *out, void *stream);
+/* grid_grad: (nexamples, nchannels, D, D, D) f32 device.
+ * coord_grad: (natoms,3) f32 device, in the frame of the prepared coordinates.
+ * type_grad: (sum over sets of atoms*T) f32 device packed like weights (vector), or NULL. */
+gm_status gm_backward(const gm_params *p, const gm_batch *b, const void *workspace,
+                      const float *grid_grad, float *coord_grad, float *type_grad,
+                      void *stream);
+/* Transformed coordinates computed by gm_prepare: (natoms,3) f64 device view. */
+const double *gm_workspace_positions(const void *workspace);
+
+/* ---- reference-shaped kernels (argument meaning as _kernels.py) ---- */
+
+/* _kernels.forward_index_sets(out, coords, radii, tidx, set_start, set_end,
+ *   set_example, set_choff, set_t, origins, res, grm, rmult, binary)
+ * out (nexamples, nch, npts^3) f32 (pre-zeroing not required: every voxel is
+ * written); coords (natoms,3) f64; radii (natoms) f64 scaled; tidx/set_* int64. */
+gm_status gm_forward_index_sets_host(float *out, int64_t nexamples, int64_t nch, int64_t npts,
+                                     const double *coords, const double *radii,
+                                     const int64_t *tidx, int64_t natoms,
+                                     const int64_t *set_start, const int64_t *set_end,
+                                     const int64_t *set_example, const int64_t *set_choff,
+                                     const int64_t *set_t, int64_t nsets,
+                                     const double *origins, double res, double grm,
+                                     double rmult, int32_t binary);
+
+/* _kernels.forward_vector_sets(out, coords, weights_flat, w_start, atom_radii,
+ *   type_radii_flat, tr_start, radius_type_indexed, set_start, set_end,
+ *   set_example, set_choff, set_t, origins, res, grm, rmult, binary) */
+gm_status gm_forward_vector_sets_host(float *out, int64_t nexamples, int64_t nch, int64_t npts,
+                                      const double *coords, int64_t natoms,
+                                      const double *weights_flat, int64_t nweights,
+                                      const int64_t *w_start, const double *atom_radii,
+                                      const double *type_radii_flat, int64_t ntype_radii,
+                                      const int64_t *tr_start, int32_t radius_type_indexed,
+                                      const int64_t *set_start, const int64_t *set_end,
+                                      const int64_t *set_example, const int64_t *set_choff,
+                                      const int64_t *set_t, int64_t nsets,
+                                      const double *origins, double res, double grm,
+                                      double rmult, int32_t binary);
+
+/* _kernels.backward_index(coords, radii, tidx, grid_grad, origin, res, grm, rmult)
+ * -> coord_grad (n,3) f64 (written to the caller's buffer). grid_grad (ntypes, npts^3) f32. */
+gm_status gm_backward_index_host(double *coord_grad, const double *coords, const double *radii,
+                                 const int64_t *tidx, int64_t n, const float *grid_grad,
+                                 int64_t ntypes, int64_t npts, const double *origin,
+                                 double res, double grm, double rmult);
+
+/* _kernels.backward_vector(coords, atom_radii, weights, grid_grad, type_radii,
+ *   radius_type_indexed, origin, res, grm, rmult) -> (coord_grad (n,3), type_grad (n,nt)) f64 */
+gm_status gm_backward_vector_host(double *coord_grad, double *type_grad, const double *coords,
+                                  const double *atom_radii, const double *weights, int64_t n,
+                                  int64_t nt, const float *grid_grad, int64_t npts,
+                                  const double *type_radii, int32_t radius_type_indexed,
+                                  const double *origin, double res, double grm, double rmult);
+
+/* ---- misc ---- */
+const char *gm_last_error(void);
+const char *gm_version(void);
+int32_t gm_device_count(void);
+/* sizeof(gm_params) (which = 0) or sizeof(gm_batch) (which = 1): ABI check for bindings. */
+int32_t gm_struct_size(int32_t which);
+/* Kernel launches issued by this process since the last reset (bench evidence). */
+int64_t gm_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRIDMAKER_B200_H */

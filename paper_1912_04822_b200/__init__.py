@@ -1,0 +1,23 @@
+"""B200-native GridMaker hot path of libmolgrid (arXiv 1912.04822).
+
+Drop-in for the gridding path of the reference ``voxmol`` package:
+``GridMaker`` (forward / forward_batch / backward, plus backward_batch and
+device-resident packed batches), the rigid ``Transform`` augmentation, and
+the ``CoordinateSet`` / ``Example`` containers.  All arithmetic runs in the
+in-tree CUDA extension (``libgridmaker_b200.so``, sm_100a) via its C ABI.
+"""
+
+from .coordsets import CoordinateSet, Example, make_vector_types
+from .errors import ConfigError, DeviceError, VoxmolError
+from .geom import (IDENTITY_QUATERNION, Quaternion, Transform, draw_transforms,
+                   make_transform, random_unit_quaternion, transform_example)
+from .voxelizer import GridMaker, channel_count, channel_names, save_grid
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "CoordinateSet", "Example", "make_vector_types", "ConfigError", "DeviceError",
+    "VoxmolError", "IDENTITY_QUATERNION", "Quaternion", "Transform", "draw_transforms",
+    "make_transform", "random_unit_quaternion", "transform_example", "GridMaker",
+    "channel_count", "channel_names", "save_grid",
+]

@@ -1,0 +1,237 @@
+"""Host-side packing of examples into one device-resident CSR batch.
+
+Restates the packing of the reference's ``GridMaker._run_batch``
+(/root/reference/pkg/src/voxmol/voxelizer.py:372-435) for the C ABI's
+``gm_batch``: atoms of every set of every example are concatenated in
+example/set order; sets own consecutive channel blocks (``set_choff``);
+radii are widened to f64 and multiplied by ``radius_scale`` on the host
+exactly like voxelizer.py:416,430; vector-mode forward items are the
+nonzero weights in atom-major, channel-minor order (_kernels.py:159-166).
+
+All static arrays live in ONE pinned host buffer mirrored by ONE device
+buffer, so (re)uploading a batch is a single host->device copy.  The
+per-call arrays (origins, transforms) are uploaded separately.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+from .errors import ConfigError
+
+_ALIGN = 256
+
+
+class _Layout:
+    def __init__(self):
+        self.arrays = []   # (name, np.ndarray)
+        self.offsets = {}
+        self.size = 0
+
+    def add(self, name, arr):
+        arr = np.ascontiguousarray(arr)
+        self.offsets[name] = (self.size, arr.dtype, arr.shape)
+        self.arrays.append((name, arr))
+        self.size += (arr.nbytes + _ALIGN - 1) // _ALIGN * _ALIGN if arr.nbytes else _ALIGN
+
+
+class PackedBatch:
+    """A batch of examples resident in device memory.
+
+    Attributes of interest: ``nexamples``, ``nchannels``, ``natoms``,
+    ``placed`` (list of (example, choff, set, atom_offset, weight_offset)),
+    ``default_centers`` (N,3) float64 (voxelizer.py:305-309 semantics).
+    """
+
+    def __init__(self, example_sets, nchannels, vector_mode, radius_scale,
+                 radius_type_indexed, device, centers=None):
+        self.device = torch.device(device)
+        self.nexamples = len(example_sets)
+        self.nchannels = int(nchannels)
+        self.vector_mode = bool(vector_mode)
+        placed = []
+        for e, sets in enumerate(example_sets):
+            choff = 0
+            for cs in sets:
+                placed.append((e, choff, cs))
+                choff += int(cs.num_types)
+        self.nsets = len(placed)
+        counts = np.array([int(cs.coords.shape[0]) for _, _, cs in placed], dtype=np.int64)
+        starts = np.zeros(self.nsets, np.int64)
+        if self.nsets:
+            starts[1:] = np.cumsum(counts)[:-1]
+        self.natoms = int(counts.sum())
+        scale = float(radius_scale)
+
+        coords = np.zeros((self.natoms, 3), np.float32)
+        radius = np.zeros(self.natoms, np.float64)
+        atom_set = np.zeros(self.natoms, np.int32)
+        set_start = starts.astype(np.int32)
+        set_end = (starts + counts).astype(np.int32)
+        set_example = np.array([p[0] for p in placed], np.int32)
+        set_choff = np.array([p[1] for p in placed], np.int32)
+        set_t = np.array([int(p[2].num_types) for p in placed], np.int32)
+        for s, (e, choff, cs) in enumerate(placed):
+            a0, a1 = starts[s], starts[s] + counts[s]
+            if a1 > a0:
+                coords[a0:a1] = cs.coords
+                radius[a0:a1] = cs.radii.astype(np.float64) * scale
+            atom_set[a0:a1] = s
+
+        L = _Layout()
+        L.add("coords32", coords)
+        L.add("atom_radius", radius)
+        L.add("atom_set", atom_set)
+        for name, arr in (("set_start", set_start), ("set_end", set_end),
+                          ("set_example", set_example), ("set_choff", set_choff),
+                          ("set_t", set_t)):
+            L.add(name, arr)
+
+        self.placed = []
+        ex_start = np.zeros(self.nexamples, np.int32)
+        ex_end = np.zeros(self.nexamples, np.int32)
+        if not self.vector_mode:
+            atom_type = np.zeros(self.natoms, np.int32)
+            for s, (e, choff, cs) in enumerate(placed):
+                a0, a1 = starts[s], starts[s] + counts[s]
+                if a1 > a0:
+                    atom_type[a0:a1] = cs.type_index
+                self.placed.append((e, choff, cs, int(a0), -1))
+            L.add("atom_type", atom_type)
+            for s in range(self.nsets):
+                e = set_example[s]
+                if s == 0 or set_example[s - 1] != e:
+                    ex_start[e] = set_start[s]
+                ex_end[e] = set_end[s]
+            self.nitems = self.natoms
+            self.nweights = 0
+        else:
+            wparts, trparts, it_atom, it_ch, it_w, it_r = [], [], [], [], [], []
+            set_wstart = np.zeros(self.nsets, np.int32)
+            set_trstart = np.zeros(self.nsets, np.int32)
+            wpos = tpos = ipos = 0
+            for s, (e, choff, cs) in enumerate(placed):
+                na, nt = int(counts[s]), int(cs.num_types)
+                a0 = int(starts[s])
+                if s == 0 or set_example[s - 1] != e:
+                    ex_start[e] = ipos
+                set_wstart[s] = wpos
+                set_trstart[s] = tpos
+                tv = (np.zeros((0, nt), np.float32) if cs.type_vector is None
+                      else np.asarray(cs.type_vector, np.float32))
+                if radius_type_indexed and na:
+                    if cs.type_radii is None:
+                        raise ConfigError(
+                            "radius_type_indexed requires coordinate sets typed from a table "
+                            "(type_radii is missing)")
+                    tr = cs.type_radii.astype(np.float64) * scale
+                else:
+                    tr = np.ones(nt, np.float64)
+                wparts.append(tv.reshape(-1))
+                trparts.append(tr)
+                if na:
+                    ia, ic = np.nonzero(tv)  # row-major: atom-major, channel-minor
+                    it_atom.append((ia + a0).astype(np.int32))
+                    it_ch.append(ic.astype(np.int32))
+                    it_w.append(tv[ia, ic].astype(np.float32))
+                    it_r.append(tr[ic] if radius_type_indexed else radius[ia + a0])
+                    ipos += ia.shape[0]
+                ex_end[e] = ipos
+                self.placed.append((e, choff, cs, a0, int(wpos)))
+                wpos += na * nt
+                tpos += nt
+            cat = (lambda parts, dt: np.concatenate(parts).astype(dt) if parts
+                   else np.zeros(0, dt))
+            L.add("weights", cat(wparts, np.float32))
+            L.add("type_radius", cat(trparts, np.float64))
+            L.add("set_wstart", set_wstart)
+            L.add("set_trstart", set_trstart)
+            L.add("item_atom", cat(it_atom, np.int32))
+            L.add("item_channel", cat(it_ch, np.int32))
+            L.add("item_weight", cat(it_w, np.float32))
+            L.add("item_radius", cat(it_r, np.float64))
+            self.nitems = int(ipos)
+            self.nweights = int(wpos)
+        L.add("ex_item_start", ex_start)
+        L.add("ex_item_end", ex_end)
+        self.offsets = L.offsets
+
+        # one pinned staging buffer -> one device buffer
+        self.host = torch.empty(L.size, dtype=torch.uint8, pin_memory=self.device.type == "cuda")
+        hb = self.host.numpy()
+        for name, arr in L.arrays:
+            off = L.offsets[name][0]
+            hb[off:off + arr.nbytes] = arr.reshape(-1).view(np.uint8)
+        self.dev = torch.empty(L.size, dtype=torch.uint8, device=self.device)
+        self.upload()
+
+        nbytes = _native.lib().gm_workspace_bytes(max(self.natoms, 1), max(self.nitems, 1))
+        self.workspace = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+        self.workspace_bytes = int(nbytes)
+        self.default_centers = np.stack([_default_center(sets) for sets in example_sets]) \
+            if self.nexamples else np.zeros((0, 3))
+        self._percall = None
+
+    # ------------------------------------------------------------------
+    @property
+    def h2d_bytes(self) -> int:
+        return int(self.host.numel())
+
+    def upload(self, non_blocking: bool = True) -> None:
+        """Copy the pinned host image to the device (one H2D copy)."""
+        self.dev.copy_(self.host, non_blocking=non_blocking)
+
+    def ptr(self, name: str) -> int | None:
+        if name not in self.offsets:
+            return None
+        return self.dev.data_ptr() + self.offsets[name][0]
+
+    def set_call_arrays(self, origins: np.ndarray, xforms: np.ndarray | None) -> None:
+        """Upload the per-call origins (N,3) and transforms (N,15), float64."""
+        n = self.nexamples
+        buf = np.zeros(n * 3 + (n * 15 if xforms is not None else 0), np.float64)
+        buf[:n * 3] = np.asarray(origins, np.float64).reshape(-1)
+        if xforms is not None:
+            buf[n * 3:] = np.asarray(xforms, np.float64).reshape(-1)
+        t = torch.from_numpy(buf)
+        if self.device.type == "cuda":
+            t = t.pin_memory()
+        self._percall = t.to(self.device, non_blocking=True)
+        self._has_xforms = xforms is not None
+
+    def gm_batch(self) -> _native.GmBatch:
+        b = _native.GmBatch()
+        b.nexamples, b.nsets, b.natoms = self.nexamples, self.nsets, self.natoms
+        b.nitems, b.nchannels, b.vector_mode = self.nitems, self.nchannels, int(self.vector_mode)
+        b.nweights = self.nweights
+        for name in ("coords32", "atom_radius", "atom_set", "atom_type", "set_start", "set_end",
+                     "set_example", "set_choff", "set_t", "set_wstart", "weights",
+                     "type_radius", "set_trstart", "item_atom", "item_channel", "item_weight",
+                     "item_radius", "ex_item_start", "ex_item_end"):
+            setattr(b, name, self.ptr(name))
+        if self._percall is None:
+            raise RuntimeError("set_call_arrays() must run before a launch")
+        base = self._percall.data_ptr()
+        b.origins = base
+        b.xforms = base + 8 * 3 * self.nexamples if self._has_xforms else None
+        return b
+
+
+def _default_center(sets) -> np.ndarray:
+    """voxelizer.py:305-309: centroid of the last non-empty set, else 0."""
+    for cs in reversed(sets):
+        if cs.coords.shape[0]:
+            return cs.coords.astype(np.float64).mean(axis=0)
+    return np.zeros(3, dtype=np.float64)
+
+
+def stream_handle(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def as_ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())

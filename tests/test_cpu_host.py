@@ -1,0 +1,277 @@
+"""CPU-only checks: the C ABI library loads and exports every declared
+symbol, the host-side mirror (geometry, validation, containers, packing)
+behaves like the reference.  No compute call needs a GPU here."""
+
+import math
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_library_exports_every_header_symbol():
+    from paper_1912_04822_b200 import _native
+
+    header = (ROOT / "include" / "gridmaker_b200.h").read_text()
+    header = re.sub(r"/\*.*?\*/", "", header, flags=re.S)
+    declared = set(re.findall(r"\b(gm_[a-z0-9_]+)\s*\(", header))
+    assert declared, "no declarations parsed"
+    L = _native.load_library()
+    for name in sorted(declared):
+        assert hasattr(L, name), f"{name} declared in the header but not exported"
+    assert set(_native.EXPORTS) == declared
+
+
+def test_abi_struct_sizes_match_bindings():
+    import ctypes
+
+    from paper_1912_04822_b200 import _native
+
+    L = _native.load_library()
+    assert L.gm_struct_size(0) == ctypes.sizeof(_native.GmParams)
+    assert L.gm_struct_size(1) == ctypes.sizeof(_native.GmBatch)
+    assert L.gm_version().startswith(b"gridmaker_b200")
+
+
+def test_workspace_bytes_monotone():
+    from paper_1912_04822_b200 import _native
+
+    L = _native.load_library()
+    a = L.gm_workspace_bytes(10, 10)
+    b = L.gm_workspace_bytes(1000, 5000)
+    assert 0 < a < b
+    assert b >= 1000 * 24 + 5000 * (64 + 32 + 16)
+
+
+def test_invalid_arguments_return_status_not_crash():
+    import ctypes
+
+    from paper_1912_04822_b200 import _native
+
+    L = _native.load_library()
+    assert L.gm_prepare(None, None, None, 0, None) == 1
+    assert b"params" in L.gm_last_error()
+    p = _native.GmParams(resolution=0.5, npts=48, radius_multiple=1.5)
+    assert L.gm_forward(ctypes.byref(p), None, None, None, None) == 1
+    assert b"batch" in L.gm_last_error()
+
+
+def test_no_cpu_fallback_without_device(monkeypatch):
+    import torch
+
+    from paper_1912_04822_b200 import DeviceError, GridMaker
+    from paper_1912_04822_b200.synthetic import ligand_only
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(DeviceError):
+        GridMaker().forward(ligand_only())
+
+
+# ---------------------------------------------------------------- geometry
+
+def test_draw_transforms_matches_sequential_make_transform():
+    from paper_1912_04822_b200 import geom
+
+    centers = np.random.default_rng(0).uniform(-3, 3, (7, 3))
+    for rot, tr in ((True, 2.0), (True, 0.0), (False, 1.5)):
+        r1, r2 = np.random.default_rng(11), np.random.default_rng(11)
+        seq = [geom.make_transform(c, tr, rot, r1) for c in centers]
+        vec = geom.draw_transforms(centers, tr, rot, r2)
+        for a, b in zip(seq, vec):
+            np.testing.assert_array_equal(a.packed(), b.packed())
+        assert r1.random() == r2.random()  # same stream position afterwards
+
+
+def test_matmul_order_calibrated():
+    from paper_1912_04822_b200 import geom
+
+    assert geom.matmul_order(1) >= 0
+    assert geom.matmul_order(50) >= 0
+
+
+def test_quaternion_basics():
+    from paper_1912_04822_b200 import Quaternion, random_unit_quaternion
+
+    q = Quaternion()
+    np.testing.assert_allclose(q.rotation_matrix(), np.eye(3), atol=1e-12)
+    assert Quaternion(2.0, 0, 0, 0).w == 1.0
+    with pytest.raises(ValueError):
+        Quaternion(0.0, 0.0, 0.0, 0.0)
+    s = math.sqrt(2.0) / 2.0
+    np.testing.assert_allclose(Quaternion(s, 0, 0, s).rotate([1.0, 0, 0]), [0, 1, 0], atol=1e-7)
+    r = random_unit_quaternion(np.random.default_rng(7))
+    np.testing.assert_allclose(r.rotation_matrix() @ r.conjugate().rotation_matrix(), np.eye(3),
+                               atol=1e-12)
+
+
+def test_mean_rotation_angle_uniform_so3():
+    from paper_1912_04822_b200 import random_unit_quaternion
+
+    rng = np.random.default_rng(2024)
+    angles = [random_unit_quaternion(rng).angle for _ in range(10_000)]
+    mean_deg = math.degrees(sum(angles) / len(angles))
+    assert abs(mean_deg - math.degrees(math.pi / 2 + 2 / math.pi)) < 2.0
+
+
+def test_transform_rigid_and_inverse():
+    from paper_1912_04822_b200 import make_transform
+
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        x = rng.uniform(-10, 10, (9, 3))
+        t = make_transform(rng.uniform(-3, 3, 3), 4.0, True, rng)
+        y = t.forward(x)
+        d0 = np.linalg.norm(x[:, None] - x[None], axis=-1)
+        d1 = np.linalg.norm(y[:, None] - y[None], axis=-1)
+        assert np.abs(d0 - d1).max() < 1e-4
+        np.testing.assert_allclose(t.inverse().forward(y), x, atol=1e-4)
+
+
+def test_transform_matches_reference_fixture():
+    from golden_io import load
+    from paper_1912_04822_b200 import Quaternion, Transform
+
+    d = load("transforms")
+    for i, pk in enumerate(d["packs"]):
+        R = pk[:9].reshape(3, 3)
+        t = Transform(Quaternion(), pk[9:12], pk[12:15])
+        object.__setattr__(t, "rotation", _FixedRotation(R))
+        np.testing.assert_array_equal(t.forward(d[f"x{i}"].astype(np.float64)), d[f"y{i}"])
+
+
+class _FixedRotation:
+    def __init__(self, R):
+        self.R = R
+
+    def rotation_matrix(self):
+        return self.R
+
+
+def test_make_transform_validation():
+    from paper_1912_04822_b200 import IDENTITY_QUATERNION, make_transform
+
+    t = make_transform((0, 0, 0), 0.0, False, np.random.default_rng(0))
+    assert t.rotation == IDENTITY_QUATERNION and not t.translation.any()
+    with pytest.raises(ValueError):
+        make_transform((0, 0, 0), -1.0, False, np.random.default_rng(0))
+    rng = np.random.default_rng(9)
+    for _ in range(50):
+        assert (np.abs(make_transform((0, 0, 0), 2.0, False, rng).translation) <= 2.0).all()
+
+
+# ---------------------------------------------------------------- containers
+
+def test_coordinate_set_invariants():
+    from paper_1912_04822_b200 import CoordinateSet, make_vector_types
+
+    with pytest.raises(ValueError):
+        CoordinateSet(coords=np.zeros((2, 3)), radii=[1.0], num_types=1, type_index=[0, 0])
+    with pytest.raises(ValueError):
+        CoordinateSet(coords=np.zeros((1, 3)), radii=[0.0], num_types=1, type_index=[0])
+    with pytest.raises(ValueError):
+        CoordinateSet(coords=np.zeros((1, 3)), radii=[1.0], num_types=1)
+    with pytest.raises(ValueError):
+        CoordinateSet(coords=np.zeros((1, 3)), radii=[1.0], num_types=2, type_index=[2])
+    with pytest.raises(ValueError):
+        CoordinateSet(coords=[[np.nan, 0, 0]], radii=[1.0], num_types=1, type_index=[0])
+    cs = CoordinateSet(coords=[[1, 2, 3], [3, 2, 1]], radii=[1, 2], num_types=3,
+                       type_index=[0, 2])
+    np.testing.assert_array_equal(cs.centroid(), [2.0, 2.0, 2.0])
+    v = make_vector_types(cs)
+    np.testing.assert_array_equal(v.type_vector, [[1, 0, 0], [0, 0, 1]])
+    with pytest.raises(ValueError):
+        make_vector_types(v)
+
+
+def test_gridmaker_host_geometry_and_params():
+    from paper_1912_04822_b200 import GridMaker
+
+    for res, dim, want in ((0.5, 23.5, 48), (1.0, 23.0, 24), (0.5, 0.0, 1), (0.25, 6.0, 25),
+                           (0.25, 23.75, 96)):
+        assert GridMaker(resolution=res, dimension=dim).points_per_side() == want
+    with pytest.raises(ValueError):
+        GridMaker(resolution=0.0).points_per_side()
+    gm = GridMaker()
+    assert gm.density(0.0, 1.0) == 1.0
+    assert abs(gm.density(1.0, 1.0) - math.exp(-2)) < 1e-12
+    assert gm.density(1.5, 1.0) == 0.0 and gm.density(1.499, 1.0) > 0.0
+    assert GridMaker(binary=True).density(0.99, 1.0) == 1.0
+    np.testing.assert_array_equal(gm.grid_origin((0, 0, 0)), [-11.75] * 3)
+    params = GridMaker(resolution=1.0, binary=True).get_params()
+    assert GridMaker().set_params(**params).get_params() == params
+    with pytest.raises(ValueError):
+        GridMaker().set_params(voxels=3)
+    with pytest.raises(ValueError):
+        GridMaker(radius_scale=-1.0).fit()
+
+
+@pytest.mark.parametrize("grm", [0.5, 1.0, 1.5, 2.0])
+@pytest.mark.parametrize("r", [0.5, 1.0, 1.9, 2.2])
+def test_density_c1_continuity(grm, r):
+    from paper_1912_04822_b200 import GridMaker
+
+    gm = GridMaker(gaussian_radius_multiple=grm)
+    d0, eps = grm * r, 1e-9
+    assert abs(gm.density(d0 - eps, r) - gm.density(d0 + eps, r)) < 1e-6
+    assert abs(gm.density_slope(d0 - eps, r) - gm.density_slope(d0 + eps, r)) < 1e-5
+
+
+def test_batch_validation_before_device():
+    """The reference's argument errors are raised before any device work."""
+    from conftest import random_coordinate_set
+    from paper_1912_04822_b200 import Example, GridMaker, make_vector_types
+
+    rng = np.random.default_rng(0)
+    gm = GridMaker()
+    with pytest.raises(ValueError):
+        gm.forward_batch([])
+    with pytest.raises(TypeError):
+        gm.forward_batch([object()])
+    a = Example([random_coordinate_set(rng, 3, 2)])
+    b = Example([random_coordinate_set(rng, 3, 3)])
+    with pytest.raises(ValueError):
+        gm.forward_batch([a, b])
+    v = Example([make_vector_types(random_coordinate_set(rng, 3, 2))])
+    with pytest.raises(ValueError):
+        gm.forward_batch([a, v])
+    with pytest.raises(ValueError):
+        gm.forward_batch([a], out=np.zeros((1, 3, 48, 48, 48), np.float32))
+    with pytest.raises(TypeError):
+        gm.forward_batch([a], out=np.zeros((1, 2, 48, 48, 48), np.float64))
+    with pytest.raises(ValueError):
+        gm.forward_batch([a], centers=np.zeros((2, 3)))
+    with pytest.raises(TypeError):
+        gm.forward(a)
+
+
+def test_packing_layout_cpu():
+    import torch
+
+    from paper_1912_04822_b200 import synthetic
+    from paper_1912_04822_b200.packing import PackedBatch
+
+    exs = synthetic.batch(3, seed=2, vector=True)
+    sets = [ex.coord_sets for ex in exs]
+    pb = PackedBatch(sets, 28, True, 1.1, True, torch.device("cpu"))
+    assert pb.natoms == 3 * 1030 and pb.nsets == 6
+    host = pb.host.numpy()
+
+    def arr(name):
+        off, dt, shape = pb.offsets[name]
+        n = int(np.prod(shape))
+        return host[off:off + n * dt.itemsize].view(dt).reshape(shape)
+
+    ia, ic, iw = arr("item_atom"), arr("item_channel"), arr("item_weight")
+    assert pb.nitems == ia.shape[0] == sum(int((cs.type_vector != 0).sum()) for s in sets for cs in s)
+    assert (np.diff(ia) >= 0).all()  # atom-major order
+    es, ee = arr("ex_item_start"), arr("ex_item_end")
+    assert es[0] == 0 and ee[-1] == pb.nitems and (es[1:] == ee[:-1]).all()
+    # radius_type_indexed: item radius = type radius * scale
+    tr = arr("item_radius")
+    np.testing.assert_allclose(tr, synthetic.TYPE_RADII[ic].astype(np.float64) * 1.1)
+    np.testing.assert_array_equal(arr("set_choff"), [0, 14] * 3)
+    np.testing.assert_array_equal(pb.default_centers[0], exs[0].coord_sets[1].centroid())

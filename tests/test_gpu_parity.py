@@ -1,0 +1,221 @@
+"""GPU parity: the CUDA path (through GridMaker -> C ABI) against the golden
+fixtures of the live reference and the CPU oracle, on the same inputs."""
+
+import numpy as np
+import pytest
+
+import oracle
+from golden_io import (BATCH_FIXTURES, SINGLE_FIXTURES, VECTOR_FIXTURES, aug_from,
+                       dense_from_sparse, examples_from, expected_grid, load, params_from,
+                       sets_from, unpack_bits)
+from parity import assert_close, to_numpy
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def gm_of(params, **kw):
+    from paper_1912_04822_b200 import GridMaker
+
+    return GridMaker(**params, **kw)
+
+
+@pytest.mark.parametrize("name", SINGLE_FIXTURES)
+def test_single_forward_golden(name):
+    d = load(name)
+    grid = gm_of(params_from(d)).forward(sets_from(d)[0], center=d["center"])
+    assert_close(grid, d["grid"], what=name)
+    if name.startswith("fwd_index"):
+        # the reference's own absolute gate (test_voxelizer.py:146)
+        assert np.abs(grid.astype(np.float64) - d["grid"]).max() < 1e-6
+
+
+@pytest.mark.parametrize("name", BATCH_FIXTURES + VECTOR_FIXTURES)
+def test_batch_forward_golden(name):
+    d = load(name)
+    p = params_from(d)
+    grid = gm_of(p).forward_batch(examples_from(d), **aug_from(d))
+    want = expected_grid(d)
+    if p["binary"]:
+        np.testing.assert_array_equal(grid, want)
+    else:
+        assert_close(grid, want, what=name)
+
+
+def test_backward_index_golden():
+    d = load("bwd_index")
+    cg, tg = gm_of(params_from(d)).backward(sets_from(d)[0], d["grid_grad"], center=d["center"])
+    assert tg is None
+    assert_close(cg, d["coord_grad"], what="bwd_index")
+
+
+@pytest.mark.parametrize("rti", [0, 1])
+def test_backward_vector_golden(rti):
+    d = load(f"bwd_vector_rti{rti}")
+    cg, tg = gm_of(params_from(d)).backward(sets_from(d)[0], d["grid_grad"], center=d["center"])
+    assert_close(cg, d["coord_grad"], what="coord")
+    assert_close(tg, d["type_grad"], what="type")
+
+
+def test_c2_example_golden_offset_frame():
+    d = load("c2_example")
+    exs = examples_from(d)
+    gm = gm_of({})
+    grid = gm.forward_batch(exs)
+    want = dense_from_sparse(d)
+    assert_close(grid, want, what="c2 forward")
+    res = gm.backward_batch(exs, want)
+    assert_close(res[0][0][0], d["coord_grad_rec"], what="c2 receptor grad")
+    assert_close(res[0][1][0], d["coord_grad_lig"], what="c2 ligand grad")
+
+
+def test_c3_example_golden_bit_exact():
+    d = load("c3_example")
+    grid = gm_of({"binary": True}).forward_batch(
+        examples_from(d), random_rotation=True, random_translation=2.0,
+        rng=np.random.default_rng(int(d["aug_seed"])))
+    np.testing.assert_array_equal(grid, unpack_bits(d))
+
+
+# ------------------------------------------------------------ full-size vs oracle
+
+def _synthetic(n, seed, vector=False, offset=None):
+    from paper_1912_04822_b200 import synthetic
+
+    return synthetic.batch(n, seed=seed, vector=vector, offset=offset)
+
+
+@pytest.mark.parametrize("offset", [False, True])
+def test_c2_batch_fwd_bwd_vs_oracle(offset):
+    from paper_1912_04822_b200 import synthetic
+
+    exs = _synthetic(50, 2, offset=synthetic.PDB_OFFSET if offset else None)
+    gm = gm_of({})
+    go = oracle.GridOracle()
+    grid, xf = gm.forward_batch(exs, random_rotation=True, random_translation=2.0,
+                                rng=np.random.default_rng(3), return_transforms=True)
+    ref = go.forward_batch(exs, random_rotation=True, random_translation=2.0,
+                           rng=np.random.default_rng(3))
+    assert_close(grid, ref, what="C2 forward")
+    gg = np.random.default_rng(7).standard_normal(grid.shape, dtype=np.float32)
+    got = gm.backward_batch(exs, gg, transforms=xf)
+    cgs, _ = go.backward_batch(exs, gg, random_rotation=True, random_translation=2.0,
+                               rng=np.random.default_rng(3))
+    flat_got = np.concatenate([c for ex in got for (c, t) in ex])
+    assert_close(flat_got, np.concatenate(cgs), what="C2 backward (N(0,1) grad)")
+    # physically shaped gradient: d(1/2 |grid|^2)/d grid = grid
+    got2 = gm.backward_batch(exs, ref, transforms=xf)
+    cgs2, _ = go.backward_batch(exs, ref, random_rotation=True, random_translation=2.0,
+                                rng=np.random.default_rng(3))
+    assert_close(np.concatenate([c for ex in got2 for (c, t) in ex]), np.concatenate(cgs2),
+                 what="C2 backward (grid grad)")
+
+
+def test_c3_batch_binary_bit_exact_vs_oracle():
+    exs = _synthetic(50, 2)
+    gm = gm_of({"binary": True})
+    go = oracle.GridOracle(binary=True)
+    grid = gm.forward_batch(exs, random_rotation=True, random_translation=2.0,
+                            rng=np.random.default_rng(0))
+    ref = go.forward_batch(exs, random_rotation=True, random_translation=2.0,
+                           rng=np.random.default_rng(0))
+    np.testing.assert_array_equal(grid, ref)
+
+
+@pytest.mark.parametrize("rti", [False, True])
+def test_c4_vector_fwd_bwd_vs_oracle(rti):
+    exs = _synthetic(12, 4, vector=True)
+    gm = gm_of({"radius_type_indexed": rti})
+    go = oracle.GridOracle(radius_type_indexed=rti)
+    grid, xf = gm.forward_batch(exs, random_rotation=True, rng=np.random.default_rng(5),
+                                return_transforms=True)
+    ref = go.forward_batch(exs, random_rotation=True, rng=np.random.default_rng(5))
+    assert_close(grid, ref, what="C4 forward")
+    gg = np.random.default_rng(7).standard_normal(grid.shape, dtype=np.float32)
+    got = gm.backward_batch(exs, gg, transforms=xf)
+    cgs, tgs = go.backward_batch(exs, gg, random_rotation=True, rng=np.random.default_rng(5))
+    assert_close(np.concatenate([c for ex in got for (c, t) in ex]), np.concatenate(cgs),
+                 what="C4 coord grad")
+    assert_close(np.concatenate([t.reshape(-1) for ex in got for (c, t) in ex]),
+                 np.concatenate([t.reshape(-1) for t in tgs]), what="C4 type grad")
+
+
+def test_c4_vector_binary_vs_oracle():
+    exs = _synthetic(6, 4, vector=True)
+    gm = gm_of({"binary": True})
+    go = oracle.GridOracle(binary=True)
+    grid = gm.forward_batch(exs, random_rotation=True, rng=np.random.default_rng(6))
+    ref = go.forward_batch(exs, random_rotation=True, rng=np.random.default_rng(6))
+    np.testing.assert_array_equal(grid, ref)
+
+
+def test_c5_fine_grid_vs_oracle():
+    exs = _synthetic(4, 2)
+    gm = gm_of({"resolution": 0.25, "dimension": 23.75})
+    assert gm.points_per_side() == 96
+    go = oracle.GridOracle(resolution=0.25, dimension=23.75)
+    grid, xf = gm.forward_batch(exs, random_rotation=True, rng=np.random.default_rng(8),
+                                return_transforms=True)
+    ref = go.forward_batch(exs, random_rotation=True, rng=np.random.default_rng(8))
+    assert_close(grid, ref, what="C5 forward")
+    gg = np.random.default_rng(9).standard_normal(grid.shape, dtype=np.float32)
+    got = gm.backward_batch(exs, gg, transforms=xf)
+    cgs, _ = go.backward_batch(exs, gg, random_rotation=True, rng=np.random.default_rng(8))
+    assert_close(np.concatenate([c for ex in got for (c, t) in ex]), np.concatenate(cgs),
+                 what="C5 backward")
+
+
+@pytest.mark.parametrize("dim,res", [(8.0, 0.5), (6.0, 0.25), (11.3, 0.7), (0.0, 0.5)])
+def test_odd_grid_sizes_vs_oracle(dim, res, rng):
+    from conftest import random_coordinate_set
+    from paper_1912_04822_b200 import Example
+
+    exs = [Example(coord_sets=[random_coordinate_set(rng, 20, 3, 5.0),
+                               random_coordinate_set(rng, 3, 2, 2.0)]) for _ in range(3)]
+    for binary in (False, True):
+        gm = gm_of({"resolution": res, "dimension": dim, "binary": binary})
+        go = oracle.GridOracle(resolution=res, dimension=dim, binary=binary)
+        grid = gm.forward_batch(exs, random_rotation=True, rng=np.random.default_rng(1))
+        ref = go.forward_batch(exs, random_rotation=True, rng=np.random.default_rng(1))
+        if binary:
+            np.testing.assert_array_equal(grid, ref)
+        else:
+            assert_close(grid, ref, what=f"D={gm.points_per_side()}")
+
+
+def test_single_atom_sets_binary_rotation_bit_exact(rng):
+    """Sets of one atom take numpy's N=1 matmul path (gemv order)."""
+    from conftest import random_coordinate_set
+    from paper_1912_04822_b200 import Example
+
+    exs = [Example(coord_sets=[random_coordinate_set(rng, 1, 2, 4.0),
+                               random_coordinate_set(rng, 2, 2, 4.0)]) for _ in range(40)]
+    gm = gm_of({"binary": True, "dimension": 12.0})
+    go = oracle.GridOracle(binary=True, dimension=12.0)
+    grid = gm.forward_batch(exs, random_rotation=True, random_translation=1.0,
+                            rng=np.random.default_rng(2))
+    ref = go.forward_batch(exs, random_rotation=True, random_translation=1.0,
+                           rng=np.random.default_rng(2))
+    np.testing.assert_array_equal(grid, ref)
+
+
+def test_device_tensor_out_and_determinism():
+    exs = _synthetic(8, 2)
+    from paper_1912_04822_b200 import GridMaker
+
+    gm = GridMaker()
+    out = torch.empty((8, 28, 48, 48, 48), device="cuda")
+    got = gm.forward_batch(exs, out=out)
+    assert got is out
+    again = gm.forward_batch(exs)
+    np.testing.assert_array_equal(to_numpy(out), again)
+    # a slab does not depend on its neighbours in the batch
+    solo = gm.forward_batch(exs[3:4])
+    np.testing.assert_array_equal(solo[0], again[3])
