@@ -89,7 +89,7 @@ typedef struct {
 } gm_batch;
 
 /* Device scratch needed by gm_prepare / gm_forward / gm_backward. */
-size_t gm_workspace_bytes(int32_t natoms, int32_t nitems);
+size_t gm_workspace_bytes(int32_t natoms, int32_t nitems, int32_t nexamples, int32_t nchannels);
 
 gm_status gm_prepare(const gm_params *p, const gm_batch *b, void *workspace,
                      size_t workspace_bytes, void *stream);

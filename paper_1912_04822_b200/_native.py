@@ -80,7 +80,7 @@ def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
             "make -C paper_1912_04822_b200/csrc)")
     L = ctypes.CDLL(str(p))
     P = ctypes.POINTER
-    L.gm_workspace_bytes.argtypes = [_c_int32, _c_int32]
+    L.gm_workspace_bytes.argtypes = [_c_int32, _c_int32, _c_int32, _c_int32]
     L.gm_workspace_bytes.restype = _c_size_t
     L.gm_prepare.argtypes = [P(GmParams), P(GmBatch), _vp, _c_size_t, _vp]
     L.gm_prepare.restype = ctypes.c_int

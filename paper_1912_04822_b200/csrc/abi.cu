@@ -1,0 +1,483 @@
+// abi.cu -- the C ABI (include/gridmaker_b200.h): argument checks, workspace
+// carving and the reference-shaped host-buffer entry points.  Nothing here
+// throws; every entry point returns a gm_status and records a message for
+// gm_last_error().
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+#define GM_VERSION "gridmaker_b200 0.2.0 (sm_100a)"
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+gm_status gm_fail(gm_status code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+void gm_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static gm_status check_params(const gm_params *p) {
+    if (!p) return gm_fail(GM_ERR_INVALID, "params is NULL");
+    if (!(p->resolution > 0)) return gm_fail(GM_ERR_INVALID, "resolution must be > 0");
+    if (p->npts < 1 || p->npts > 4096) return gm_fail(GM_ERR_INVALID, "npts %d out of range", p->npts);
+    if (!(p->radius_multiple > 0)) return gm_fail(GM_ERR_INVALID, "radius_multiple must be > 0");
+    return GM_OK;
+}
+
+static gm_status check_batch(const gm_batch *b) {
+    if (!b) return gm_fail(GM_ERR_INVALID, "batch is NULL");
+    if (b->nexamples < 0 || b->nsets < 0 || b->natoms < 0 || b->nitems < 0 || b->nchannels < 0)
+        return gm_fail(GM_ERR_INVALID, "negative batch size");
+    if (b->natoms > 0 && !b->coords32 && !b->coords64)
+        return gm_fail(GM_ERR_INVALID, "batch has atoms but no coordinates");
+    if (b->natoms > 0 && (!b->atom_set || !b->atom_radius || !b->set_example || !b->set_choff ||
+                          !b->set_start || !b->set_end || !b->set_t))
+        return gm_fail(GM_ERR_INVALID, "batch is missing atom/set arrays");
+    if (b->nexamples > 0 && (!b->origins || !b->ex_item_start || !b->ex_item_end))
+        return gm_fail(GM_ERR_INVALID, "batch is missing per-example arrays");
+    if (b->nexamples > 65535) return gm_fail(GM_ERR_INVALID, "too many examples per launch");
+    if (b->nchannels > 8192) return gm_fail(GM_ERR_INVALID, "too many channels");
+    return GM_OK;
+}
+
+extern "C" size_t gm_workspace_bytes(int32_t natoms, int32_t nitems, int32_t nexamples,
+                                     int32_t nchannels) {
+    return carve_workspace(nullptr, natoms, nitems, nexamples, nchannels, nullptr);
+}
+
+static Workspace ws_of(const void *workspace, const gm_batch *b) {
+    Workspace w;
+    carve_workspace(const_cast<void *>(workspace), b->natoms, b->nitems, b->nexamples,
+                    b->nchannels, &w);
+    return w;
+}
+
+extern "C" const double *gm_workspace_positions(const void *workspace) {
+    return (const double *)workspace;  // positions are carved first
+}
+
+extern "C" gm_status gm_prepare(const gm_params *p, const gm_batch *b, void *workspace,
+                                size_t workspace_bytes, void *stream) {
+    gm_status st = check_params(p);
+    if (st) return st;
+    if ((st = check_batch(b))) return st;
+    const size_t need = gm_workspace_bytes(b->natoms, b->nitems, b->nexamples, b->nchannels);
+    if (!workspace || workspace_bytes < need)
+        return gm_fail(GM_ERR_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, need);
+    if (!b->vector_mode && b->nitems != b->natoms)
+        return gm_fail(GM_ERR_INVALID, "index mode needs one item per atom");
+    if (b->nitems > 0 && !b->item_channel && !b->atom_type)
+        return gm_fail(GM_ERR_INVALID, "items need item_channel or atom_type");
+    return prepare_impl(p, b, ws_of(workspace, b), (cudaStream_t)stream, true);
+}
+
+extern "C" gm_status gm_forward(const gm_params *p, const gm_batch *b, const void *workspace,
+                                float *out, void *stream) {
+    gm_status st = check_params(p);
+    if (st) return st;
+    if ((st = check_batch(b))) return st;
+    if (b->nexamples == 0 || b->nchannels == 0) return GM_OK;
+    if (!out) return gm_fail(GM_ERR_INVALID, "out is NULL");
+    if (!workspace) return gm_fail(GM_ERR_INVALID, "workspace is NULL");
+    return forward_impl(p, b, ws_of(workspace, b), out, (cudaStream_t)stream);
+}
+
+extern "C" gm_status gm_backward(const gm_params *p, const gm_batch *b, const void *workspace,
+                                 const float *grid_grad, float *coord_grad, float *type_grad,
+                                 void *stream) {
+    gm_status st = check_params(p);
+    if (st) return st;
+    if ((st = check_batch(b))) return st;
+    if (b->natoms == 0) return GM_OK;
+    if (!coord_grad) return gm_fail(GM_ERR_INVALID, "coord_grad is NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p->binary) {
+        // voxelizer.py:284-289: binary grids are flat almost everywhere
+        CUDA_TRY(cudaMemsetAsync(coord_grad, 0, sizeof(float) * 3 * (size_t)b->natoms, s));
+        if (b->vector_mode && type_grad && b->nweights > 0)
+            CUDA_TRY(cudaMemsetAsync(type_grad, 0, sizeof(float) * (size_t)b->nweights, s));
+        return GM_OK;
+    }
+    if (!grid_grad || !workspace) return gm_fail(GM_ERR_INVALID, "grid_grad/workspace is NULL");
+    if (!b->vector_mode && !b->atom_type) return gm_fail(GM_ERR_INVALID, "atom_type is NULL");
+    if (b->vector_mode && (!b->weights || !b->set_wstart))
+        return gm_fail(GM_ERR_INVALID, "vector backward needs weights and set_wstart");
+    if (b->vector_mode && p->radius_type_indexed && (!b->type_radius || !b->set_trstart))
+        return gm_fail(GM_ERR_INVALID, "radius_type_indexed needs type_radius and set_trstart");
+    return backward_impl(p, b, ws_of(workspace, b), grid_grad, coord_grad, type_grad, s);
+}
+
+// ----------------------------------------------------------------------------
+// reference-shaped host entry points (numpy buffers in, numpy buffers out)
+// ----------------------------------------------------------------------------
+namespace {
+
+struct DevBuf {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+    ~DevBuf() {
+        if (ptr) cudaFree(ptr);
+    }
+    cudaError_t reserve(size_t n) {
+        if (n <= bytes) return cudaSuccess;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&ptr, n);
+        if (e == cudaSuccess) bytes = n;
+        return e;
+    }
+};
+
+// Staging arena for the *_host entry points: one growable device buffer per
+// thread, carved into the arrays of one call.
+struct Arena {
+    DevBuf buf;
+};
+
+thread_local Arena t_arena;
+
+struct HostPlan {
+    std::vector<std::pair<size_t, std::pair<const void *, size_t>>> uploads;
+    size_t used = 0;
+    size_t add(const void *src, size_t bytes) {
+        size_t off = used;
+        used = align_up(used + std::max<size_t>(bytes, 1), 256);
+        if (src) uploads.push_back({off, {src, bytes}});
+        return off;
+    }
+};
+
+}  // namespace
+
+static gm_status run_host_forward(float *out, int64_t nexamples, int64_t nch, int64_t npts,
+                                  const double *coords, int64_t natoms,
+                                  const std::vector<int32_t> &atom_set,
+                                  const std::vector<int32_t> &atom_type,
+                                  const std::vector<double> &atom_radius,
+                                  const std::vector<int32_t> &item_atom,
+                                  const std::vector<int32_t> &item_channel,
+                                  const std::vector<float> &item_weight,
+                                  const std::vector<double> &item_radius, bool vector_mode,
+                                  const std::vector<int32_t> *sets /* 5 arrays */,
+                                  const std::vector<int32_t> &ex_start,
+                                  const std::vector<int32_t> &ex_end, const double *origins,
+                                  const gm_params &p) {
+    const int32_t nsets = (int32_t)sets[0].size();
+    const int32_t nitems = vector_mode ? (int32_t)item_atom.size() : (int32_t)natoms;
+    HostPlan plan;
+    const size_t o_coords = plan.add(coords, sizeof(double) * 3 * natoms);
+    const size_t o_aset = plan.add(atom_set.data(), 4 * atom_set.size());
+    const size_t o_atype = plan.add(atom_type.data(), 4 * atom_type.size());
+    const size_t o_arad = plan.add(atom_radius.data(), 8 * atom_radius.size());
+    size_t o_sets[5];
+    for (int k = 0; k < 5; k++) o_sets[k] = plan.add(sets[k].data(), 4 * sets[k].size());
+    const size_t o_iatom = plan.add(item_atom.data(), 4 * item_atom.size());
+    const size_t o_ich = plan.add(item_channel.data(), 4 * item_channel.size());
+    const size_t o_iw = plan.add(item_weight.data(), 4 * item_weight.size());
+    const size_t o_irad = plan.add(item_radius.data(), 8 * item_radius.size());
+    const size_t o_exs = plan.add(ex_start.data(), 4 * ex_start.size());
+    const size_t o_exe = plan.add(ex_end.data(), 4 * ex_end.size());
+    const size_t o_orig = plan.add(origins, sizeof(double) * 3 * nexamples);
+    const size_t ws_bytes = gm_workspace_bytes((int32_t)natoms, nitems, (int32_t)nexamples, (int32_t)nch);
+    const size_t o_ws = plan.add(nullptr, ws_bytes);
+    const size_t out_bytes = sizeof(float) * (size_t)nexamples * nch * npts * npts * npts;
+    const size_t o_out = plan.add(nullptr, out_bytes);
+
+    Arena &ar = t_arena;
+    CUDA_TRY(ar.buf.reserve(plan.used));
+    char *d = (char *)ar.buf.ptr;
+    for (auto &u : plan.uploads)
+        CUDA_TRY(cudaMemcpy(d + u.first, u.second.first, u.second.second, cudaMemcpyHostToDevice));
+    gm_batch b;
+    memset(&b, 0, sizeof b);
+    b.nexamples = (int32_t)nexamples;
+    b.nsets = nsets;
+    b.natoms = (int32_t)natoms;
+    b.nitems = nitems;
+    b.nchannels = (int32_t)nch;
+    b.vector_mode = vector_mode;
+    b.coords64 = (const double *)(d + o_coords);
+    b.atom_set = (const int32_t *)(d + o_aset);
+    b.atom_type = atom_type.empty() ? nullptr : (const int32_t *)(d + o_atype);
+    b.atom_radius = (const double *)(d + o_arad);
+    b.set_start = (const int32_t *)(d + o_sets[0]);
+    b.set_end = (const int32_t *)(d + o_sets[1]);
+    b.set_example = (const int32_t *)(d + o_sets[2]);
+    b.set_choff = (const int32_t *)(d + o_sets[3]);
+    b.set_t = (const int32_t *)(d + o_sets[4]);
+    if (vector_mode) {
+        b.item_atom = (const int32_t *)(d + o_iatom);
+        b.item_channel = (const int32_t *)(d + o_ich);
+        b.item_weight = (const float *)(d + o_iw);
+        b.item_radius = (const double *)(d + o_irad);
+    }
+    b.ex_item_start = (const int32_t *)(d + o_exs);
+    b.ex_item_end = (const int32_t *)(d + o_exe);
+    b.origins = (const double *)(d + o_orig);
+    gm_status st = gm_prepare(&p, &b, d + o_ws, ws_bytes, nullptr);
+    if (st) return st;
+    st = gm_forward(&p, &b, d + o_ws, (float *)(d + o_out), nullptr);
+    if (st) return st;
+    CUDA_TRY(cudaMemcpy(out, d + o_out, out_bytes, cudaMemcpyDeviceToHost));
+    return GM_OK;
+}
+
+static gm_params host_params(int64_t npts, double res, double grm, double rmult, int32_t binary,
+                             int32_t rti) {
+    gm_params p;
+    memset(&p, 0, sizeof p);
+    p.resolution = res;
+    p.dimension = res * (double)(npts - 1);
+    p.radius_scale = 1.0;
+    p.gaussian_radius_multiple = grm;
+    p.radius_multiple = rmult;
+    p.npts = (int32_t)npts;
+    p.binary = binary;
+    p.radius_type_indexed = rti;
+    p.matmul_order_1 = -1;
+    p.matmul_order_n = -1;
+    return p;
+}
+
+// Validates the reference's packing invariants (voxelizer.py:372-388): sets of
+// one example are consecutive and atoms are packed in set order.
+static gm_status pack_sets(int64_t nsets, int64_t nexamples, int64_t natoms,
+                           const int64_t *set_start, const int64_t *set_end,
+                           const int64_t *set_example, const int64_t *set_choff,
+                           const int64_t *set_t, std::vector<int32_t> *sets,
+                           std::vector<int32_t> &atom_set) {
+    for (int k = 0; k < 5; k++) sets[k].resize(nsets);
+    atom_set.assign(natoms, 0);
+    int64_t prev_e = 0;
+    for (int64_t s = 0; s < nsets; s++) {
+        if (set_start[s] < 0 || set_end[s] > natoms || set_end[s] < set_start[s])
+            return gm_fail(GM_ERR_INVALID, "set %lld has a bad atom range", (long long)s);
+        if (set_example[s] < prev_e || set_example[s] >= nexamples)
+            return gm_fail(GM_ERR_INVALID, "sets must be grouped by example in order");
+        prev_e = set_example[s];
+        sets[0][s] = (int32_t)set_start[s];
+        sets[1][s] = (int32_t)set_end[s];
+        sets[2][s] = (int32_t)set_example[s];
+        sets[3][s] = (int32_t)set_choff[s];
+        sets[4][s] = (int32_t)set_t[s];
+        for (int64_t a = set_start[s]; a < set_end[s]; a++) atom_set[a] = (int32_t)s;
+    }
+    return GM_OK;
+}
+
+extern "C" gm_status gm_forward_index_sets_host(
+    float *out, int64_t nexamples, int64_t nch, int64_t npts, const double *coords,
+    const double *radii, const int64_t *tidx, int64_t natoms, const int64_t *set_start,
+    const int64_t *set_end, const int64_t *set_example, const int64_t *set_choff,
+    const int64_t *set_t, int64_t nsets, const double *origins, double res, double grm,
+    double rmult, int32_t binary) {
+    if (!out || (natoms && (!coords || !radii || !tidx)) || !origins)
+        return gm_fail(GM_ERR_INVALID, "NULL argument");
+    std::vector<int32_t> sets[5], atom_set;
+    gm_status st = pack_sets(nsets, nexamples, natoms, set_start, set_end, set_example, set_choff,
+                             set_t, sets, atom_set);
+    if (st) return st;
+    std::vector<int32_t> atom_type(natoms);
+    for (int64_t a = 0; a < natoms; a++) atom_type[a] = (int32_t)tidx[a];
+    std::vector<double> atom_radius(radii, radii + natoms);
+    std::vector<int32_t> ex_start(nexamples, 0), ex_end(nexamples, 0);
+    for (int64_t s = 0; s < nsets; s++) {
+        const int64_t e = set_example[s];
+        if (ex_end[e] == ex_start[e]) ex_start[e] = (int32_t)set_start[s];
+        ex_end[e] = (int32_t)set_end[s];
+    }
+    gm_params p = host_params(npts, res, grm, rmult, binary, 0);
+    static const std::vector<int32_t> ei;
+    static const std::vector<float> ef;
+    static const std::vector<double> ed;
+    return run_host_forward(out, nexamples, nch, npts, coords, natoms, atom_set, atom_type,
+                            atom_radius, ei, ei, ef, ed, false, sets, ex_start, ex_end, origins, p);
+}
+
+extern "C" gm_status gm_forward_vector_sets_host(
+    float *out, int64_t nexamples, int64_t nch, int64_t npts, const double *coords,
+    int64_t natoms, const double *weights_flat, int64_t nweights, const int64_t *w_start,
+    const double *atom_radii, const double *type_radii_flat, int64_t ntype_radii,
+    const int64_t *tr_start, int32_t radius_type_indexed, const int64_t *set_start,
+    const int64_t *set_end, const int64_t *set_example, const int64_t *set_choff,
+    const int64_t *set_t, int64_t nsets, const double *origins, double res, double grm,
+    double rmult, int32_t binary) {
+    if (!out || !origins || (natoms && (!coords || !weights_flat || !atom_radii)))
+        return gm_fail(GM_ERR_INVALID, "NULL argument");
+    std::vector<int32_t> sets[5], atom_set;
+    gm_status st = pack_sets(nsets, nexamples, natoms, set_start, set_end, set_example, set_choff,
+                             set_t, sets, atom_set);
+    if (st) return st;
+    std::vector<int32_t> item_atom, item_channel;
+    std::vector<float> item_weight;
+    std::vector<double> item_radius;
+    std::vector<int32_t> ex_start(nexamples, 0), ex_end(nexamples, 0);
+    std::vector<char> seen(nexamples, 0);
+    for (int64_t s = 0; s < nsets; s++) {
+        const int64_t e = set_example[s], nt = set_t[s];
+        if (!seen[e]) {
+            ex_start[e] = (int32_t)item_atom.size();
+            seen[e] = 1;
+        }
+        for (int64_t a = set_start[s]; a < set_end[s]; a++) {
+            for (int64_t c = 0; c < nt; c++) {
+                const int64_t wi = w_start[s] + (a - set_start[s]) * nt + c;
+                if (wi < 0 || wi >= nweights) return gm_fail(GM_ERR_INVALID, "weight index out of range");
+                const double w = weights_flat[wi];
+                if (w == 0.0) continue;  // _kernels.py:164
+                double r = atom_radii[a];
+                if (radius_type_indexed) {
+                    const int64_t ti = tr_start[s] + c;
+                    if (!type_radii_flat || ti < 0 || ti >= ntype_radii)
+                        return gm_fail(GM_ERR_INVALID, "type radius index out of range");
+                    r = type_radii_flat[ti];
+                }
+                item_atom.push_back((int32_t)a);
+                item_channel.push_back((int32_t)c);
+                item_weight.push_back((float)w);
+                item_radius.push_back(r);
+            }
+        }
+        ex_end[e] = (int32_t)item_atom.size();
+    }
+    std::vector<double> atom_radius(atom_radii, atom_radii + natoms);
+    std::vector<int32_t> atom_type;
+    gm_params p = host_params(npts, res, grm, rmult, binary, radius_type_indexed);
+    return run_host_forward(out, nexamples, nch, npts, coords, natoms, atom_set, atom_type,
+                            atom_radius, item_atom, item_channel, item_weight, item_radius, true,
+                            sets, ex_start, ex_end, origins, p);
+}
+
+static gm_status run_host_backward(double *coord_grad, double *type_grad, const double *coords,
+                                   const double *radii, const int64_t *tidx,
+                                   const double *weights, int64_t n, int64_t nt,
+                                   const float *grid_grad, int64_t npts, const double *type_radii,
+                                   int32_t rti, const double *origin, double res, double grm,
+                                   double rmult) {
+    if (n == 0) return GM_OK;
+    const bool vector_mode = weights != nullptr;
+    std::vector<int32_t> atom_set(n, 0), atom_type;
+    if (!vector_mode) {
+        atom_type.resize(n);
+        for (int64_t a = 0; a < n; a++) atom_type[a] = (int32_t)tidx[a];
+    }
+    std::vector<float> w32;
+    if (vector_mode) w32.assign(weights, weights + n * nt);
+    const int32_t set_start = 0, set_end = (int32_t)n, set_example = 0, set_choff = 0,
+                  set_t = (int32_t)nt, set_ws = 0, set_tr = 0;
+    const int32_t ex_s = 0, ex_e = (int32_t)n;
+    const size_t D3 = (size_t)npts * npts * npts;
+    HostPlan plan;
+    const size_t o_coords = plan.add(coords, sizeof(double) * 3 * n);
+    const size_t o_rad = plan.add(radii, sizeof(double) * n);
+    const size_t o_aset = plan.add(atom_set.data(), 4 * n);
+    const size_t o_atype = plan.add(atom_type.data(), 4 * atom_type.size());
+    const size_t o_ss = plan.add(&set_start, 4), o_se = plan.add(&set_end, 4),
+                 o_sx = plan.add(&set_example, 4), o_sc = plan.add(&set_choff, 4),
+                 o_st = plan.add(&set_t, 4), o_sw = plan.add(&set_ws, 4),
+                 o_str = plan.add(&set_tr, 4);
+    const size_t o_w = plan.add(w32.data(), 4 * w32.size());
+    const size_t o_tr = plan.add(type_radii, type_radii ? sizeof(double) * nt : 0);
+    const size_t o_exs = plan.add(&ex_s, 4), o_exe = plan.add(&ex_e, 4);
+    const size_t o_orig = plan.add(origin, sizeof(double) * 3);
+    const size_t o_gg = plan.add(grid_grad, sizeof(float) * nt * D3);
+    const size_t ws_bytes = gm_workspace_bytes((int32_t)n, (int32_t)n, 1, (int32_t)nt);
+    const size_t o_ws = plan.add(nullptr, ws_bytes);
+    const size_t o_cg = plan.add(nullptr, sizeof(float) * 3 * n);
+    const size_t o_tg = plan.add(nullptr, sizeof(float) * (vector_mode ? n * nt : 1));
+    Arena &ar = t_arena;
+    CUDA_TRY(ar.buf.reserve(plan.used));
+    char *d = (char *)ar.buf.ptr;
+    for (auto &u : plan.uploads)
+        CUDA_TRY(cudaMemcpy(d + u.first, u.second.first, u.second.second, cudaMemcpyHostToDevice));
+    gm_batch b;
+    memset(&b, 0, sizeof b);
+    b.nexamples = 1;
+    b.nsets = 1;
+    b.natoms = (int32_t)n;
+    b.nitems = (int32_t)n;
+    b.nchannels = (int32_t)nt;
+    b.vector_mode = vector_mode;
+    b.coords64 = (const double *)(d + o_coords);
+    b.atom_radius = (const double *)(d + o_rad);
+    b.atom_set = (const int32_t *)(d + o_aset);
+    b.atom_type = vector_mode ? nullptr : (const int32_t *)(d + o_atype);
+    b.set_start = (const int32_t *)(d + o_ss);
+    b.set_end = (const int32_t *)(d + o_se);
+    b.set_example = (const int32_t *)(d + o_sx);
+    b.set_choff = (const int32_t *)(d + o_sc);
+    b.set_t = (const int32_t *)(d + o_st);
+    b.set_wstart = (const int32_t *)(d + o_sw);
+    b.set_trstart = (const int32_t *)(d + o_str);
+    b.nweights = vector_mode ? (int32_t)(n * nt) : 0;
+    b.weights = vector_mode ? (const float *)(d + o_w) : nullptr;
+    b.type_radius = type_radii ? (const double *)(d + o_tr) : nullptr;
+    b.item_channel = nullptr;
+    b.ex_item_start = (const int32_t *)(d + o_exs);
+    b.ex_item_end = (const int32_t *)(d + o_exe);
+    b.origins = (const double *)(d + o_orig);
+    gm_params p = host_params(npts, res, grm, rmult, 0, rti);
+    // positions only (no transform); items are not needed by the backward
+    gm_status st = prepare_impl(&p, &b, ws_of(d + o_ws, &b), nullptr, false);
+    if (st) return st;
+    st = gm_backward(&p, &b, d + o_ws, (const float *)(d + o_gg), (float *)(d + o_cg),
+                               vector_mode ? (float *)(d + o_tg) : nullptr, nullptr);
+    if (st) return st;
+    std::vector<float> cg(3 * n), tg(vector_mode ? n * nt : 0);
+    CUDA_TRY(cudaMemcpy(cg.data(), d + o_cg, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < 3 * n; i++) coord_grad[i] = cg[i];
+    if (vector_mode) {
+        CUDA_TRY(cudaMemcpy(tg.data(), d + o_tg, sizeof(float) * n * nt, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n * nt; i++) type_grad[i] = tg[i];
+    }
+    return GM_OK;
+}
+
+extern "C" gm_status gm_backward_index_host(double *coord_grad, const double *coords,
+                                            const double *radii, const int64_t *tidx, int64_t n,
+                                            const float *grid_grad, int64_t ntypes, int64_t npts,
+                                            const double *origin, double res, double grm,
+                                            double rmult) {
+    if (n && (!coord_grad || !coords || !radii || !tidx || !grid_grad || !origin))
+        return gm_fail(GM_ERR_INVALID, "NULL argument");
+    return run_host_backward(coord_grad, nullptr, coords, radii, tidx, nullptr, n, ntypes,
+                             grid_grad, npts, nullptr, 0, origin, res, grm, rmult);
+}
+
+extern "C" gm_status gm_backward_vector_host(double *coord_grad, double *type_grad,
+                                             const double *coords, const double *atom_radii,
+                                             const double *weights, int64_t n, int64_t nt,
+                                             const float *grid_grad, int64_t npts,
+                                             const double *type_radii, int32_t rti,
+                                             const double *origin, double res, double grm,
+                                             double rmult) {
+    if (n && (!coord_grad || !type_grad || !coords || !atom_radii || !weights || !grid_grad ||
+              !origin || (rti && !type_radii)))
+        return gm_fail(GM_ERR_INVALID, "NULL argument");
+    return run_host_backward(coord_grad, type_grad, coords, atom_radii, nullptr, weights, n, nt,
+                             grid_grad, npts, type_radii, rti, origin, res, grm, rmult);
+}
+
+extern "C" const char *gm_last_error(void) { return g_err.c_str(); }
+extern "C" const char *gm_version(void) { return GM_VERSION; }
+extern "C" int32_t gm_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+extern "C" int32_t gm_struct_size(int32_t which) {
+    return which == 0 ? (int32_t)sizeof(gm_params) : which == 1 ? (int32_t)sizeof(gm_batch) : -1;
+}
+extern "C" int64_t gm_launch_count(int32_t reset) {
+    return reset ? g_launches.exchange(0) : g_launches.load();
+}

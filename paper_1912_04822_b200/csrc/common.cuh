@@ -1,0 +1,137 @@
+// common.cuh -- records, workspace layout and device helpers shared by the
+// gridding kernels (prepare.cu, forward.cu, backward.cu) and the C ABI (abi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+
+#include "../../include/gridmaker_b200.h"
+
+// ---------------------------------------------------------------------------
+// error plumbing (abi.cu)
+// ---------------------------------------------------------------------------
+gm_status gm_fail(gm_status code, const char *fmt, ...);
+void gm_count_launch();
+
+#define CUDA_TRY(expr)                                                                       \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess)                                                               \
+            return gm_fail(GM_ERR_CUDA, "%s failed: %s (%s:%d)", #expr,                      \
+                           cudaGetErrorString(_e), __FILE__, __LINE__);                      \
+    } while (0)
+
+#define LAUNCH_CHECK()                                                                       \
+    do {                                                                                     \
+        gm_count_launch();                                                                   \
+        cudaError_t _e = cudaGetLastError();                                                 \
+        if (_e != cudaSuccess)                                                               \
+            return gm_fail(GM_ERR_CUDA, "kernel launch failed: %s (%s:%d)",                  \
+                           cudaGetErrorString(_e), __FILE__, __LINE__);                      \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// device records
+// ---------------------------------------------------------------------------
+// One forward item: index mode -> an atom; vector mode -> an (atom, channel)
+// pair with nonzero weight (_kernels.py:159-166).  64 B = 4 x LDS.128.
+struct __align__(16) FwdItem {
+    float xh, yh, zh, cexp;  // grid-local coordinate x - origin (hi part); -2 log2(e) / r^2
+    float xl, yl, zl, d02;   // lo parts (x - origin = hi + lo to ~2^-48); (grm r)^2
+    float dzr, qa, w;        // cutoff rmult*r; quadratic coefficient; weight
+    int ch;                  // absolute output channel
+    int ibox, jbox, kbox;    // voxel box per axis: lo | hi << 16 (_kernels.py:22-30)
+    int atom;                // packed atom index
+};
+static_assert(sizeof(FwdItem) == 64, "FwdItem must be 64 bytes");
+
+// Exact binary-mode record: transformed f64 position and r^2 (_kernels.py:81,95-98).
+struct __align__(16) BinItem {
+    double x, y, z, r2;
+};
+
+__host__ __device__ inline int box_lo(int b) { return b & 0xffff; }
+__host__ __device__ inline int box_hi(int b) { return b >> 16; }
+
+// ---------------------------------------------------------------------------
+// workspace: one caller-provided device buffer
+// ---------------------------------------------------------------------------
+struct Workspace {
+    double *pos;         // natoms * 3: transformed f64 coordinates
+    FwdItem *items;      // nitems, packed order
+    BinItem *bitems;     // nitems, packed order
+    int32_t *item_ch;    // nitems: channel, or -1 when the box misses the grid
+    FwdItem *sorted;     // nitems: per example, grouped by channel in item order
+    BinItem *bsorted;    // nitems (binary mode)
+    int32_t *chan_off;   // nexamples * (nchannels + 1): ranges into sorted
+};
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+inline size_t carve_workspace(void *base, int32_t natoms, int32_t nitems, int32_t nex,
+                              int32_t nch, Workspace *w) {
+    char *p = (char *)base;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        char *q = p ? p + off : nullptr;
+        off = align_up(off + std::max<size_t>(bytes, 16), 256);
+        return q;
+    };
+    const size_t na = (size_t)std::max(natoms, 1), ni = (size_t)std::max(nitems, 1);
+    Workspace tmp;
+    Workspace *ws = w ? w : &tmp;
+    ws->pos = (double *)take(sizeof(double) * 3 * na);
+    ws->items = (FwdItem *)take(sizeof(FwdItem) * ni);
+    ws->bitems = (BinItem *)take(sizeof(BinItem) * ni);
+    ws->item_ch = (int32_t *)take(sizeof(int32_t) * ni);
+    ws->sorted = (FwdItem *)take(sizeof(FwdItem) * ni);
+    ws->bsorted = (BinItem *)take(sizeof(BinItem) * ni);
+    ws->chan_off = (int32_t *)take(sizeof(int32_t) * (size_t)std::max(nex, 1) * (nch + 1));
+    return off + 256;
+}
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+// _kernels.py:22-30 in f64 with the reference's operation order:
+//   lo = ceil(((x - cut) - origin) / res), hi = floor(((x + cut) - origin) / res),
+// clamped to [0, D-1] (the clamp keeps lo > hi for boxes that miss the grid).
+__device__ __forceinline__ void axis_bounds(double x, double cut, double origin, double res,
+                                            int D, int &lo, int &hi) {
+    double l = ceil(__ddiv_rn(__dsub_rn(__dsub_rn(x, cut), origin), res));
+    double h = floor(__ddiv_rn(__dsub_rn(__dadd_rn(x, cut), origin), res));
+    l = fmin(fmax(l, 0.0), (double)D);
+    h = fmax(fmin(h, (double)(D - 1)), -1.0);
+    lo = (int)l;
+    hi = (int)h;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// floor(a / b) for 0 <= a < 64, 1 <= b <= 64 without an integer divide:
+// (a + 0.5) / b is at least 1/128 away from an integer.
+__device__ __forceinline__ int small_div(int a, float inv_b) {
+    return (int)(((float)a + 0.5f) * inv_b);
+}
+
+// ---------------------------------------------------------------------------
+// host-side implementation entry points (used by abi.cu)
+// ---------------------------------------------------------------------------
+gm_status prepare_impl(const gm_params *p, const gm_batch *b, const Workspace &ws,
+                       cudaStream_t s, bool items_too);
+gm_status forward_impl(const gm_params *p, const gm_batch *b, const Workspace &ws, float *out,
+                       cudaStream_t s);
+gm_status backward_impl(const gm_params *p, const gm_batch *b, const Workspace &ws,
+                        const float *grid_grad, float *coord_grad, float *type_grad,
+                        cudaStream_t s);

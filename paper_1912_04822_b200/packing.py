@@ -169,7 +169,8 @@ class PackedBatch:
         self.dev = torch.empty(L.size, dtype=torch.uint8, device=self.device)
         self.upload()
 
-        nbytes = _native.lib().gm_workspace_bytes(max(self.natoms, 1), max(self.nitems, 1))
+        nbytes = _native.lib().gm_workspace_bytes(max(self.natoms, 1), max(self.nitems, 1),
+                                                   max(self.nexamples, 1), self.nchannels)
         self.workspace = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
         self.workspace_bytes = int(nbytes)
         self.default_centers = np.stack([_default_center(sets) for sets in example_sets]) \

@@ -192,7 +192,8 @@ class GridMaker:
 
     def pack(self, examples, nchannels=None, device=None, check_type_radii=True) -> PackedBatch:
         """Pack examples (CoordinateSets or Examples) into a device-resident batch."""
-        example_sets = [coord_sets_of(ex) for ex in examples]
+        example_sets = [list(ex) if isinstance(ex, (list, tuple)) else coord_sets_of(ex)
+                        for ex in examples]
         vector_mode = _batch_mode(example_sets)
         if nchannels is None:
             nchannels = max([sum(int(cs.num_types) for cs in s) for s in example_sets] or [0])

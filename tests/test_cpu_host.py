@@ -40,10 +40,10 @@ def test_workspace_bytes_monotone():
     from paper_1912_04822_b200 import _native
 
     L = _native.load_library()
-    a = L.gm_workspace_bytes(10, 10)
-    b = L.gm_workspace_bytes(1000, 5000)
+    a = L.gm_workspace_bytes(10, 10, 1, 28)
+    b = L.gm_workspace_bytes(1000, 5000, 50, 28)
     assert 0 < a < b
-    assert b >= 1000 * 24 + 5000 * (64 + 32 + 16)
+    assert b >= 1000 * 24 + 5000 * (64 + 32 + 4 + 64 + 32) + 50 * 29 * 4
 
 
 def test_invalid_arguments_return_status_not_crash():
