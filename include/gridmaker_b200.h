@@ -83,6 +83,7 @@ typedef struct {
     const float *item_weight;        /* (nitems) or NULL = 1 */
     const double *item_radius;       /* (nitems) scaled radius, or NULL = atom_radius */
     const int32_t *ex_item_start, *ex_item_end; /* (nexamples) */
+    int32_t max_example_items;       /* max over examples of (ex_item_end - ex_item_start) */
     /* per example */
     const double *origins;           /* (nexamples,3) center - dimension/2 */
     const double *xforms;            /* (nexamples,15) R row-major, center, translation; NULL = none */

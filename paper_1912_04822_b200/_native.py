@@ -53,7 +53,7 @@ class GmBatch(ctypes.Structure):
         ("set_t", _vp), ("set_wstart", _vp), ("weights", _vp), ("nweights", _c_int32),
         ("type_radius", _vp), ("set_trstart", _vp),
         ("item_atom", _vp), ("item_channel", _vp), ("item_weight", _vp), ("item_radius", _vp),
-        ("ex_item_start", _vp), ("ex_item_end", _vp),
+        ("ex_item_start", _vp), ("ex_item_end", _vp), ("max_example_items", _c_int32),
         ("origins", _vp), ("xforms", _vp),
     ]
 

@@ -25,6 +25,20 @@ gm_status gm_fail(gm_status code, const char *fmt, ...) {
 
 void gm_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+cudaError_t gm_ensure_smem(const void *func, int bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<int, const void *>, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto &d : done)
+        if (d.first.first == dev && d.first.second == func && d.second >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.push_back({{dev, func}, bytes});
+    return e;
+}
+
 static gm_status check_params(const gm_params *p) {
     if (!p) return gm_fail(GM_ERR_INVALID, "params is NULL");
     if (!(p->resolution > 0)) return gm_fail(GM_ERR_INVALID, "resolution must be > 0");
@@ -223,6 +237,9 @@ static gm_status run_host_forward(float *out, int64_t nexamples, int64_t nch, in
     }
     b.ex_item_start = (const int32_t *)(d + o_exs);
     b.ex_item_end = (const int32_t *)(d + o_exe);
+    b.max_example_items = 0;
+    for (size_t e = 0; e < ex_start.size(); e++)
+        b.max_example_items = std::max(b.max_example_items, ex_end[e] - ex_start[e]);
     b.origins = (const double *)(d + o_orig);
     gm_status st = gm_prepare(&p, &b, d + o_ws, ws_bytes, nullptr);
     if (st) return st;
@@ -425,6 +442,7 @@ static gm_status run_host_backward(double *coord_grad, double *type_grad, const 
     b.item_channel = nullptr;
     b.ex_item_start = (const int32_t *)(d + o_exs);
     b.ex_item_end = (const int32_t *)(d + o_exe);
+    b.max_example_items = (int32_t)n;
     b.origins = (const double *)(d + o_orig);
     gm_params p = host_params(npts, res, grm, rmult, 0, rti);
     // positions only (no transform); items are not needed by the backward

@@ -82,9 +82,18 @@ __device__ __forceinline__ double offs(double x, double o, int i, double res) {
     return __dsub_rn(x, __dadd_rn(o, __dmul_rn((double)i, res)));
 }
 
-// Walk the box of one atom for one channel.  F(ii, d2, dx, dy, dz, Exyz, g)
+// 1/sqrt(d2) to ~1e-13: f32 MUFU estimate + one f64 Newton step.
+__device__ __forceinline__ double rsqrt_d(double d2) {
+    const double y0 = (double)rsqrtf((float)d2);
+    const double e = fma(-d2 * y0, y0, 1.0);
+    return fma(0.5 * y0, e, y0);
+}
+
+// Walk the box of one atom for one channel.  f(slot, d2, dx, dy, dz, Exyz, g)
 // is called for every voxel with 0 <= d2 < dzr2 (d2 > 0 when SKIP_CENTER)
-// and g != 0, in a fixed order per lane.
+// and g != 0, in a fixed order per lane; `slot` alternates so callers can keep
+// two independent accumulator chains.  Eight loads per lane are issued before
+// any is consumed.
 template <bool SKIP_CENTER, typename F>
 __device__ __forceinline__ void walk_box(const AtomGeom &G, const Tables &T, const float *gbase,
                                          int D, double dzr2, int lane, F &&f) {
@@ -103,23 +112,27 @@ __device__ __forceinline__ void walk_box(const AtomGeom &G, const Tables &T, con
             const double dyz2 = fma(dy, dy, dz2);
             const double eyz = G.direct ? 1.0 : T.ey[jj] * ez;
             const float *gp = gbase + ((size_t)G.i0 * D + (G.j0 + jj)) * D + (G.k0 + kk);
-            for (int i0 = 0; i0 < G.ni; i0 += 4) {
-                float g[4];
-                double d2[4], dx[4];
+            for (int i0 = 0; i0 < G.ni; i0 += 8) {
+                float g[8];
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
+                for (int q = 0; q < 8; q++) {
                     const int ii = i0 + q;
-                    dx[q] = ii < G.ni ? (G.direct ? offs(G.x, G.ox, G.i0 + ii, G.res) : T.dx[ii]) : 0.0;
-                    d2[q] = ii < G.ni ? fma(dx[q], dx[q], dyz2) : dzr2;
-                    const bool in = (SKIP_CENTER ? d2[q] > 0.0 : true) && d2[q] < dzr2;
+                    bool in = false;
+                    if (ii < G.ni) {
+                        const double dx = G.direct ? offs(G.x, G.ox, G.i0 + ii, G.res) : T.dx[ii];
+                        const double d2 = fma(dx, dx, dyz2);
+                        in = (SKIP_CENTER ? d2 > 0.0 : true) && d2 < dzr2;
+                    }
                     g[q] = in ? __ldg(gp + (size_t)ii * plane) : 0.0f;
                 }
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
+                for (int q = 0; q < 8; q++) {
                     if (g[q] != 0.0f) {
                         const int ii = i0 + q;
-                        const double exyz = G.direct ? exp(G.m2inv_r2 * d2[q]) : T.ex[ii] * eyz;
-                        f(ii, d2[q], dx[q], dy, dz, exyz, (double)g[q]);
+                        const double dx = G.direct ? offs(G.x, G.ox, G.i0 + ii, G.res) : T.dx[ii];
+                        const double d2 = fma(dx, dx, dyz2);
+                        const double exyz = G.direct ? exp(G.m2inv_r2 * d2) : T.ex[ii] * eyz;
+                        f(q & 1, d2, dx, dy, dz, exyz, (double)g[q]);
                     }
                 }
             }
@@ -127,7 +140,7 @@ __device__ __forceinline__ void walk_box(const AtomGeom &G, const Tables &T, con
     }
 }
 
-__global__ void __launch_bounds__(256) k_backward_index(const BwdArgs A) {
+__global__ void __launch_bounds__(256, 3) k_backward_index(const BwdArgs A) {
     __shared__ Tables tabs[kWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int a = blockIdx.x * kWarps + warp;
@@ -153,25 +166,31 @@ __global__ void __launch_bounds__(256) k_backward_index(const BwdArgs A) {
     const double q0 = (2.0 * grm) / r;
     const double qa2 = 2.0 * (exp((-2.0 * grm) * grm) * (q0 * q0));
     const double m4inv_r2 = -4.0 * inv_r2;
-    double gx = 0.0, gy = 0.0, gz = 0.0;
+    double ax0 = 0.0, ay0 = 0.0, az0 = 0.0, ax1 = 0.0, ay1 = 0.0, az1 = 0.0;
     Tables &T = tabs[warp];
     if (build_tables(G, dzr, -2.0 * inv_r2, res, D, T, lane)) {
         const float *gbase = A.grid_grad + ((size_t)e * b.nchannels + c) * ((size_t)D * D * D);
         walk_box<true>(G, T, gbase, D, dzr2, lane,
-                       [&](int, double d2, double dx, double dy, double dz, double exyz, double g) {
-                           double sc;
-                           if (d2 <= d02) {
-                               // slope / d = exp(-2 d^2/r^2) * (-4/r^2)
-                               sc = g * exyz * m4inv_r2;
+                       [&](int slot, double d2, double dx, double dy, double dz, double exyz,
+                           double g) {
+                           // slope / d: Gaussian exp(-2 d^2/r^2) * (-4/r^2) (no sqrt);
+                           // tail 2 qa (d - dzr) / d
+                           const double rd = rsqrt_d(d2);
+                           const double sq = g * (qa2 * fma(d2, rd, -dzr)) * rd;
+                           const double sg = g * exyz * m4inv_r2;
+                           const double sc = d2 <= d02 ? sg : sq;
+                           if (slot) {
+                               ax1 = fma(sc, dx, ax1);
+                               ay1 = fma(sc, dy, ay1);
+                               az1 = fma(sc, dz, az1);
                            } else {
-                               const double rd = rsqrt(d2);
-                               sc = g * (qa2 * fma(d2, rd, -dzr)) * rd;
+                               ax0 = fma(sc, dx, ax0);
+                               ay0 = fma(sc, dy, ay0);
+                               az0 = fma(sc, dz, az0);
                            }
-                           gx = fma(sc, dx, gx);
-                           gy = fma(sc, dy, gy);
-                           gz = fma(sc, dz, gz);
                        });
     }
+    double gx = ax0 + ax1, gy = ay0 + ay1, gz = az0 + az1;
     gx = warp_sum(gx);
     gy = warp_sum(gy);
     gz = warp_sum(gz);
@@ -250,7 +269,7 @@ __global__ void __launch_bounds__(256) k_backward_vector(const BwdArgs A) {
                             dens = G.direct ? exp(G.m2inv_r2 * d2) : T.ex[ii] * eyz;
                             sod = dens * m4inv_r2;
                         } else {
-                            const double rd = rsqrt(d2);
+                            const double rd = rsqrt_d(d2);
                             const double t = fma(d2, rd, -dzr);
                             dens = (qa * t) * t;
                             sod = (2.0 * qa) * t * rd;
@@ -303,7 +322,7 @@ __global__ void __launch_bounds__(256) k_backward_vector(const BwdArgs A) {
                                         dens = exyz;
                                         sod = dens * m4inv_r2;
                                     } else {
-                                        const double rd = rsqrt(d2);
+                                        const double rd = rsqrt_d(d2);
                                         const double t = fma(d2, rd, -dzr);
                                         dens = (qa * t) * t;
                                         sod = (2.0 * qa) * t * rd;

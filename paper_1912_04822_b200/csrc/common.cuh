@@ -19,6 +19,8 @@
 // ---------------------------------------------------------------------------
 gm_status gm_fail(gm_status code, const char *fmt, ...);
 void gm_count_launch();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel, size).
+cudaError_t gm_ensure_smem(const void *func, int bytes);
 
 #define CUDA_TRY(expr)                                                                       \
     do {                                                                                     \
@@ -43,9 +45,9 @@ void gm_count_launch();
 // One forward item: index mode -> an atom; vector mode -> an (atom, channel)
 // pair with nonzero weight (_kernels.py:159-166).  64 B = 4 x LDS.128.
 struct __align__(16) FwdItem {
-    float xh, yh, zh, cexp;  // grid-local coordinate x - origin (hi part); -2 log2(e) / r^2
-    float xl, yl, zl, d02;   // lo parts (x - origin = hi + lo to ~2^-48); (grm r)^2
-    float dzr, qa, w;        // cutoff rmult*r; quadratic coefficient; weight
+    float cxh, cyh, czh, cexp;  // offset voxel(box corner) - atom per axis, hi part; -2 log2(e)/r^2
+    float cxl, cyl, czl, d02;   // lo parts (offset = hi + lo to ~2^-48); (grm r)^2
+    float dzr, qa, w;           // cutoff (rmult*r, or r in binary mode); quadratic coeff.; weight
     int ch;                  // absolute output channel
     int ibox, jbox, kbox;    // voxel box per axis: lo | hi << 16 (_kernels.py:22-30)
     int atom;                // packed atom index

@@ -33,7 +33,7 @@ struct FwdArgs {
     const double *origins;
     float *out;
     double res;
-    float resf;
+    float resf, resl, inv_res;  // res = resf + resl
     int D, C, TI, TJ, ntj, wpp, rpw;
     int bulk;
     size_t acc_floats;
@@ -44,6 +44,113 @@ __device__ __forceinline__ void bulk_store(float *gdst, const float *ssrc, uint3
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s),
                  "r"(bytes)
                  : "memory");
+}
+
+// Ex2 / sqrt on the MUFU unit (no denormal / special-case paths: arguments
+// are finite, d^2 >= 0, densities >= 2^-126 where they matter).
+__device__ __forceinline__ float fast_ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float fast_sqrt(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Conservative index range [lo, hi] (relative to the box corner) of voxels
+// whose axis offset c + idx*res lies in [-rho, rho].
+__device__ __forceinline__ void sphere_span(float c, float rho, float inv_res, int n, int &lo,
+                                            int &hi) {
+    const float a = (-rho - c) * inv_res, b = (rho - c) * inv_res;
+    lo = max(0, (int)ceilf(fmaxf(a, -1.0f)));
+    hi = min(n - 1, (int)floorf(fminf(b, (float)n)));
+}
+
+// One item's contribution to a warp's region (plane i, rows [jg0, jg1]):
+// the voxels of its box cross-section that can lie inside its cutoff sphere.
+// Lane -> (row offset r, column kk), column fixed per item.
+template <bool BINARY, bool VECTOR>
+__device__ __forceinline__ void visit_item(const FwdItem &it, const BinItem &bi, int i, int jg0,
+                                           int jg1, float *accw, int D, double res, float resf,
+                                           float resl, float inv_res, double ox, double oy,
+                                           double oz, int lane) {
+    const int4 bx = *reinterpret_cast<const int4 *>(&it.ibox);
+    const int ilo = box_lo(bx.x);
+    if (i < ilo || i > box_hi(bx.x)) return;
+    const int jlo_b = box_lo(bx.y), klo_b = box_lo(bx.z);
+    const int jlo = max(jlo_b, jg0), jhi = min(box_hi(bx.y), jg1);
+    if (jlo > jhi) return;
+    const float4 P = *reinterpret_cast<const float4 *>(&it.cxh);
+    const float4 Q = *reinterpret_cast<const float4 *>(&it.cxl);
+    const float4 R = *reinterpret_cast<const float4 *>(&it.dzr);
+    const float cut = R.x;
+    // plane offset dx (f32, ~1 ulp) and the sphere cross-section radius
+    const float fi = (float)(i - ilo);
+    const float dx = fmaf(fi, resf, P.x) + fmaf(fi, resl, Q.x);
+    const float rho2 = fmaf(-dx, dx, cut * cut);
+    if (rho2 < -1e-5f * cut * cut) return;
+    const float rho = fmaf(fast_sqrt(fmaxf(rho2, 0.0f)), 1.00002f, 1e-4f * cut);
+    int jr0, jr1, kr0, kr1;
+    sphere_span(P.y + Q.y, rho, inv_res, box_hi(bx.y) - jlo_b + 1, jr0, jr1);
+    sphere_span(P.z + Q.z, rho, inv_res, box_hi(bx.z) - klo_b + 1, kr0, kr1);
+    jr0 = max(jr0, jlo - jlo_b);
+    jr1 = min(jr1, jhi - jlo_b);
+    if (jr0 > jr1 || kr0 > kr1) return;
+    const int nj = jr1 - jr0 + 1, nk = kr1 - kr0 + 1;
+    float *arow = accw + (size_t)(jlo_b + jr0) * D + klo_b;
+    if (BINARY) {
+        // _kernels.py:87-98 (index) / 180-192 (vector): exact f64, no contraction
+        const float w = R.z;
+        const double dxd = __dsub_rn(__dadd_rn(ox, __dmul_rn((double)i, res)), bi.x);
+        const double dx2 = __dmul_rn(dxd, dxd);
+        for (int kb = 0; kb < nk; kb += 32) {
+            const int nks = min(32, nk - kb);
+            const float inv = __frcp_rn((float)nks);
+            const int rpi = small_div(32, inv);
+            const int r = small_div(lane, inv), kk = kr0 + kb + lane - r * nks;
+            if (r >= rpi) continue;
+            const double dz = __dsub_rn(__dadd_rn(oz, __dmul_rn((double)(klo_b + kk), res)), bi.z);
+            const double dz2 = __dmul_rn(dz, dz);
+            float *ap = arow + kk + (size_t)r * D;
+            for (int jj = r; jj < nj; jj += rpi, ap += (size_t)rpi * D) {
+                const double dy = __dsub_rn(
+                    __dadd_rn(oy, __dmul_rn((double)(jlo_b + jr0 + jj), res)), bi.y);
+                const double d2 = __dadd_rn(__dadd_rn(dx2, __dmul_rn(dy, dy)), dz2);
+                if (d2 <= bi.r2) {
+                    if (VECTOR) *ap = fmaxf(*ap, w);
+                    else *ap = 1.0f;
+                }
+            }
+        }
+    } else {
+        // _kernels.py:99-106: Gaussian core to d0, quadratic tail to the cutoff
+        const float cexp = P.w, d02 = Q.w, qa = R.y, w = R.z;
+        const float dx2 = dx * dx;
+        for (int kb = 0; kb < nk; kb += 32) {
+            const int nks = min(32, nk - kb);
+            const float inv = __frcp_rn((float)nks);
+            const int rpi = small_div(32, inv);
+            const int r = small_div(lane, inv), kk = kr0 + kb + lane - r * nks;
+            if (r >= rpi) continue;
+            const float fk = (float)kk;
+            const float dz = fmaf(fk, resf, P.z) + fmaf(fk, resl, Q.z);
+            const float b2 = fmaf(dz, dz, dx2);
+            const float rpif = (float)rpi;
+            float *ap = arow + kk + (size_t)r * D;
+            float jf = (float)(jr0 + r);
+            for (int jj = r; jj < nj; jj += rpi, jf += rpif, ap += (size_t)rpi * D) {
+                const float dy = fmaf(jf, resf, P.y) + fmaf(jf, resl, Q.y);
+                const float d2 = fmaf(dy, dy, b2);
+                const float g = fast_ex2(d2 * cexp);
+                const float t = fmaxf(cut - fast_sqrt(d2), 0.0f);
+                const float v = d2 <= d02 ? g : qa * t * t;
+                *ap = fmaf(w, v, *ap);
+            }
+        }
+    }
+    __syncwarp();
 }
 
 template <bool BINARY, bool VECTOR>
@@ -92,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const FwdArgs A) {
     const bool region_ok = p < TIv && jg0 <= jg1;
     float *accw = acc + (size_t)p * TJ * D - (size_t)j0 * D;  // accw[j * D + k]
     const double res = A.res;
-    const float resf = A.resf;
+    const float resf = A.resf, resl = A.resl, inv_res = A.inv_res;
     const double ox = A.origins[3 * e + 0], oy = A.origins[3 * e + 1], oz = A.origins[3 * e + 2];
     const int ti_hi = i0 + TIv - 1, tj_hi = j0 + TJv - 1;
     const unsigned lt = (1u << lane) - 1u;
@@ -126,77 +233,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const FwdArgs A) {
         __syncthreads();
         if (count > kCap - kThreads || base + kThreads >= ce) {
             if (region_ok) {
-                for (int idx = 0; idx < count; idx++) {
-                    const int4 bx = *reinterpret_cast<const int4 *>(&list[idx].ibox);
-                    if (i < box_lo(bx.x) || i > box_hi(bx.x)) continue;
-                    const int jlo = max(box_lo(bx.y), jg0), jhi = min(box_hi(bx.y), jg1);
-                    if (jlo > jhi) continue;
-                    const int klo = box_lo(bx.z), nk = box_hi(bx.z) - klo + 1;
-                    const int nj = jhi - jlo + 1;
-                    float *arow = accw + (size_t)jlo * D + klo;
-                    if (BINARY) {
-                        // _kernels.py:87-98 (index) / 180-192 (vector): exact f64, no contraction
-                        const BinItem bi = blist[idx];
-                        const float w = list[idx].w;
-                        const double dx = __dsub_rn(__dadd_rn(ox, __dmul_rn((double)i, res)), bi.x);
-                        const double dx2 = __dmul_rn(dx, dx);
-                        for (int kb = 0; kb < nk; kb += 32) {
-                            const int nks = min(32, nk - kb);
-                            const float inv = __frcp_rn((float)nks);
-                            const int rpi = small_div(32, inv);
-                            const int r = small_div(lane, inv), kk = kb + lane - r * nks;
-                            if (r >= rpi) continue;
-                            const double dz = __dsub_rn(
-                                __dadd_rn(oz, __dmul_rn((double)(klo + kk), res)), bi.z);
-                            const double dz2 = __dmul_rn(dz, dz);
-                            float *ap = arow + kk + (size_t)r * D;
-                            for (int jj = r; jj < nj; jj += rpi, ap += (size_t)rpi * D) {
-                                const double dy = __dsub_rn(
-                                    __dadd_rn(oy, __dmul_rn((double)(jlo + jj), res)), bi.y);
-                                const double d2 =
-                                    __dadd_rn(__dadd_rn(dx2, __dmul_rn(dy, dy)), dz2);
-                                if (d2 <= bi.r2) {
-                                    if (VECTOR) *ap = fmaxf(*ap, w);
-                                    else *ap = 1.0f;
-                                }
-                            }
-                        }
-                    } else {
-                        const float4 P = *reinterpret_cast<const float4 *>(&list[idx].xh);
-                        const float4 Q = *reinterpret_cast<const float4 *>(&list[idx].xl);
-                        const float4 R = *reinterpret_cast<const float4 *>(&list[idx].dzr);
-                        const float cexp = P.w, d02 = Q.w, dzr = R.x, qa = R.y, w = R.z;
-                        // per-item offsets in f64 (exact for any resolution); the row and
-                        // column offsets keep a lo part so dy, dz stay within ~1 ulp
-                        const float dx = (float)((double)i * res - ((double)P.x + (double)Q.x));
-                        const double dy0d = (double)jlo * res - ((double)P.y + (double)Q.y);
-                        const double dz0d = (double)klo * res - ((double)P.z + (double)Q.z);
-                        const float dy0 = (float)dy0d, dy0l = (float)(dy0d - (double)dy0);
-                        const float dz0 = (float)dz0d, dz0l = (float)(dz0d - (double)dz0);
-                        const float dx2 = dx * dx;
-                        for (int kb = 0; kb < nk; kb += 32) {
-                            const int nks = min(32, nk - kb);
-                            const float inv = __frcp_rn((float)nks);
-                            const int rpi = small_div(32, inv);
-                            const int r = small_div(lane, inv), kk = kb + lane - r * nks;
-                            if (r >= rpi) continue;
-                            const float dz = fmaf((float)kk, resf, dz0) + dz0l;
-                            const float b2 = fmaf(dz, dz, dx2);
-                            const float rpif = (float)rpi;
-                            float *ap = arow + kk + (size_t)r * D;
-                            float jf = (float)r;
-                            for (int jj = r; jj < nj; jj += rpi, jf += rpif, ap += (size_t)rpi * D) {
-                                const float dy = fmaf(jf, resf, dy0) + dy0l;
-                                const float d2 = fmaf(dy, dy, b2);
-                                const float g = exp2f(d2 * cexp);
-                                const float t = fmaxf(dzr - sqrtf(d2), 0.0f);
-                                const float v = d2 <= d02 ? g : qa * t * t;
-                                *ap = fmaf(w, v, *ap);
-                            }
-                        }
-                    }
-                    __syncwarp();
-                }
+                for (int idx = 0; idx < count; idx++)
+                    visit_item<BINARY, VECTOR>(list[idx], blist[idx], i, jg0, jg1, accw, D, res,
+                                               resf, resl, inv_res, ox, oy, oz, lane);
             }
             __syncthreads();
             count = 0;
@@ -247,11 +286,7 @@ FwdConfig choose_config(int D, bool binary) {
 template <bool BIN, bool VEC>
 gm_status launch(const FwdArgs &A, const FwdConfig &cfg, int nex, cudaStream_t s) {
     auto kern = k_forward<BIN, VEC>;
-    static int smem_set = 0;  // per instantiation; the attribute is per function
-    if ((int)cfg.smem > smem_set) {
-        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem));
-        smem_set = (int)cfg.smem;
-    }
+    CUDA_TRY(gm_ensure_smem((const void *)kern, (int)cfg.smem));
     const int ntiles = ((A.D + cfg.TI - 1) / cfg.TI) * A.ntj;
     dim3 grid(ntiles * A.C, nex);
     kern<<<grid, kThreads, cfg.smem, s>>>(A);
@@ -274,6 +309,8 @@ gm_status forward_impl(const gm_params *p, const gm_batch *b, const Workspace &w
     A.out = out;
     A.res = p->resolution;
     A.resf = (float)p->resolution;
+    A.resl = (float)(p->resolution - (double)A.resf);
+    A.inv_res = (float)(1.0 / p->resolution);
     A.D = D;
     A.C = b->nchannels;
     A.TI = cfg.TI;

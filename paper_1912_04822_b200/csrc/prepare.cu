@@ -95,14 +95,15 @@ __global__ void __launch_bounds__(256) k_prepare_items(const PrepArgs A) {
         axis_bounds(z, cut, oz, res, D, k0, k1);
         const bool valid = i0 <= i1 && j0 <= j1 && k0 <= k1;
         FwdItem f;
-        split_hilo(x - ox, f.xh, f.xl);
-        split_hilo(y - oy, f.yh, f.yl);
-        split_hilo(z - oz, f.zh, f.zl);
+        // offsets (o + lo*res) - x of the box-corner voxel, as hi + lo floats
+        split_hilo((double)i0 * res - (x - ox), f.cxh, f.cxl);
+        split_hilo((double)j0 * res - (y - oy), f.cyh, f.cyl);
+        split_hilo((double)k0 * res - (z - oz), f.czh, f.czl);
         const double r2 = r * r;
         f.cexp = (float)((-2.0 * CUDART_L2E) / r2);
         const double gr = grm * r;
         f.d02 = (float)(gr * gr);
-        f.dzr = (float)(rmult * r);
+        f.dzr = (float)cut;
         const double q0 = (2.0 * grm) / r;
         f.qa = (float)(exp((-2.0 * grm) * grm) * (q0 * q0));
         f.w = w;
@@ -134,42 +135,48 @@ struct BinArgs {
 };
 
 __global__ void __launch_bounds__(1024) k_bin(const BinArgs A) {
-    extern __shared__ int cnt[];  // C + 1
+    // smem: C+1 ints of counts/offsets, then the example's item channels
+    extern __shared__ int sh[];
+    int *cnt = sh;
+    int *chs = sh + A.C + 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int e = blockIdx.x;
     const int is = A.ex_item_start[e], ie = A.ex_item_end[e];
+    const int n = ie - is;
     const unsigned lt = (1u << lane) - 1u;
+    for (int q = threadIdx.x; q < n; q += blockDim.x) chs[q] = A.item_ch[is + q];
+    __syncthreads();
     for (int c = warp; c < A.C; c += nw) {
-        int n = 0;
-        for (int base = is; base < ie; base += 32) {
-            const int it = base + lane;
-            n += __popc(__ballot_sync(0xffffffffu, it < ie && A.item_ch[it] == c));
+        int k = 0;
+        for (int base = 0; base < n; base += 32) {
+            const int q = base + lane;
+            k += __popc(__ballot_sync(0xffffffffu, q < n && chs[q] == c));
         }
-        if (lane == 0) cnt[c] = n;
+        if (lane == 0) cnt[c] = k;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         int pos = is;
         int32_t *off = A.chan_off + (size_t)e * (A.C + 1);
         for (int c = 0; c < A.C; c++) {
-            const int n = cnt[c];
+            const int k = cnt[c];
             cnt[c] = pos;
             off[c] = pos;
-            pos += n;
+            pos += k;
         }
         off[A.C] = pos;
     }
     __syncthreads();
     for (int c = warp; c < A.C; c += nw) {
         int pos = cnt[c];
-        for (int base = is; base < ie; base += 32) {
-            const int it = base + lane;
-            const bool keep = it < ie && A.item_ch[it] == c;
+        for (int base = 0; base < n; base += 32) {
+            const int q = base + lane;
+            const bool keep = q < n && chs[q] == c;
             const unsigned m = __ballot_sync(0xffffffffu, keep);
             if (keep) {
                 const int dst = pos + __popc(m & lt);
-                A.sorted[dst] = A.items[it];
-                if (A.binary) A.bsorted[dst] = A.bitems[it];
+                A.sorted[dst] = A.items[is + q];
+                if (A.binary) A.bsorted[dst] = A.bitems[is + q];
             }
             pos += __popc(m);
         }
@@ -205,8 +212,11 @@ gm_status prepare_impl(const gm_params *p, const gm_batch *b, const Workspace &w
         B.chan_off = ws.chan_off;
         B.C = b->nchannels;
         B.binary = p->binary;
-        const size_t smem = sizeof(int) * (size_t)(b->nchannels + 1);
-        if (smem > 48 * 1024) return gm_fail(GM_ERR_INVALID, "too many channels (%d)", b->nchannels);
+        if (b->max_example_items < 0) return gm_fail(GM_ERR_INVALID, "max_example_items < 0");
+        const size_t smem = sizeof(int) * (size_t)(b->nchannels + 1 + b->max_example_items);
+        if (smem > 200 * 1024)
+            return gm_fail(GM_ERR_INVALID, "too many items per example (%d)", b->max_example_items);
+        if (smem > 48 * 1024) CUDA_TRY(gm_ensure_smem((const void *)k_bin, (int)smem));
         k_bin<<<b->nexamples, 1024, smem, s>>>(B);
         LAUNCH_CHECK();
     }

@@ -156,6 +156,7 @@ class PackedBatch:
             L.add("item_radius", cat(it_r, np.float64))
             self.nitems = int(ipos)
             self.nweights = int(wpos)
+        self.max_example_items = int((ex_end - ex_start).max()) if self.nexamples else 0
         L.add("ex_item_start", ex_start)
         L.add("ex_item_end", ex_end)
         self.offsets = L.offsets
@@ -209,6 +210,7 @@ class PackedBatch:
         b.nexamples, b.nsets, b.natoms = self.nexamples, self.nsets, self.natoms
         b.nitems, b.nchannels, b.vector_mode = self.nitems, self.nchannels, int(self.vector_mode)
         b.nweights = self.nweights
+        b.max_example_items = self.max_example_items
         for name in ("coords32", "atom_radius", "atom_set", "atom_type", "set_start", "set_end",
                      "set_example", "set_choff", "set_t", "set_wstart", "weights",
                      "type_radius", "set_trstart", "item_atom", "item_channel", "item_weight",
