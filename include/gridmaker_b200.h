@@ -151,6 +151,17 @@ gm_status gm_backward_vector_host(double *coord_grad, double *type_grad, const d
                                   const double *type_radii, int32_t radius_type_indexed,
                                   const double *origin, double res, double grm, double rmult);
 
+/* ---- host helpers ---- */
+
+/* geom.make_transform for n examples from pre-drawn uniforms (geom.py:66-76,
+ * 121-136): u is (n, k) row-major with k = 3*(rotation) + 3*(translation>0),
+ * exactly rng.random((n, k)).  Writes out (n, 15): R row-major (the
+ * quaternion's rotation_matrix, geom.py:50-57), center, translation
+ * (-t + 2t*u).  Same IEEE expressions and libm calls as the Python reference,
+ * so rows are bit-identical to the reference's draws. */
+gm_status gm_draw_transforms(const double *u, int64_t n, int32_t rotation, double translation,
+                             const double *centers, double *out);
+
 /* ---- misc ---- */
 const char *gm_last_error(void);
 const char *gm_version(void);

@@ -2,6 +2,7 @@
 // carving and the reference-shaped host-buffer entry points.  Nothing here
 // throws; every entry point returns a gm_status and records a message for
 // gm_last_error().
+#include <math.h>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -484,6 +485,51 @@ extern "C" gm_status gm_backward_vector_host(double *coord_grad, double *type_gr
         return gm_fail(GM_ERR_INVALID, "NULL argument");
     return run_host_backward(coord_grad, type_grad, coords, atom_radii, nullptr, weights, n, nt,
                              grid_grad, npts, type_radii, rti, origin, res, grm, rmult);
+}
+
+extern "C" gm_status gm_draw_transforms(const double *u, int64_t n, int32_t rotation,
+                                        double translation, const double *centers,
+                                        double *out) {
+    if (n < 0 || (n > 0 && (!out || !centers))) return gm_fail(GM_ERR_INVALID, "NULL argument");
+    const int k = (rotation ? 3 : 0) + (translation > 0 ? 3 : 0);
+    if (n > 0 && k > 0 && !u) return gm_fail(GM_ERR_INVALID, "uniforms are NULL");
+    const double tau = 2.0 * M_PI;
+    for (int64_t e = 0; e < n; e++) {
+        const double *ue = u + e * k;
+        double *o = out + e * 15;
+        if (rotation) {
+            // geom.py:73-76 (Shoemake) and 28-36 (renormalise if |n-1| > 1e-6)
+            const double a = sqrt(1.0 - ue[0]), b = sqrt(ue[0]);
+            const double t2 = tau * ue[1], t3 = tau * ue[2];
+            double w = b * cos(t3), x = a * sin(t2), y = a * cos(t2), z = b * sin(t3);
+            const double nrm = sqrt(((pow(w, 2.0) + pow(x, 2.0)) + pow(y, 2.0)) + pow(z, 2.0));
+            if (fabs(nrm - 1.0) > 1e-6) {
+                w /= nrm;
+                x /= nrm;
+                y /= nrm;
+                z /= nrm;
+            }
+            // geom.py:53-57
+            o[0] = 1.0 - 2.0 * (y * y + z * z);
+            o[1] = 2.0 * (x * y - z * w);
+            o[2] = 2.0 * (x * z + y * w);
+            o[3] = 2.0 * (x * y + z * w);
+            o[4] = 1.0 - 2.0 * (x * x + z * z);
+            o[5] = 2.0 * (y * z - x * w);
+            o[6] = 2.0 * (x * z - y * w);
+            o[7] = 2.0 * (y * z + x * w);
+            o[8] = 1.0 - 2.0 * (x * x + y * y);
+        } else {
+            for (int q = 0; q < 9; q++) o[q] = (q % 4 == 0) ? 1.0 : 0.0;
+        }
+        o[9] = centers[3 * e];
+        o[10] = centers[3 * e + 1];
+        o[11] = centers[3 * e + 2];
+        const int c = rotation ? 3 : 0;
+        for (int q = 0; q < 3; q++)
+            o[12 + q] = translation > 0 ? -translation + (2.0 * translation) * ue[c + q] : 0.0;
+    }
+    return GM_OK;
 }
 
 extern "C" const char *gm_last_error(void) { return g_err.c_str(); }

@@ -135,7 +135,8 @@ struct BinArgs {
 };
 
 __global__ void __launch_bounds__(1024) k_bin(const BinArgs A) {
-    // smem: C+1 ints of counts/offsets, then the example's item channels
+    // smem: C+1 channel offsets, then per item its channel and its rank
+    // among the example's earlier items of the same channel
     extern __shared__ int sh[];
     int *cnt = sh;
     int *chs = sh + A.C + 1;
@@ -143,14 +144,19 @@ __global__ void __launch_bounds__(1024) k_bin(const BinArgs A) {
     const int e = blockIdx.x;
     const int is = A.ex_item_start[e], ie = A.ex_item_end[e];
     const int n = ie - is;
+    int *rank = chs + n;
     const unsigned lt = (1u << lane) - 1u;
     for (int q = threadIdx.x; q < n; q += blockDim.x) chs[q] = A.item_ch[is + q];
     __syncthreads();
+    // warp w ranks the items of channels w, w+32, ... (ordered ballot scan)
     for (int c = warp; c < A.C; c += nw) {
         int k = 0;
         for (int base = 0; base < n; base += 32) {
             const int q = base + lane;
-            k += __popc(__ballot_sync(0xffffffffu, q < n && chs[q] == c));
+            const bool mine = q < n && chs[q] == c;
+            const unsigned m = __ballot_sync(0xffffffffu, mine);
+            if (mine) rank[q] = k + __popc(m & lt);
+            k += __popc(m);
         }
         if (lane == 0) cnt[c] = k;
     }
@@ -167,19 +173,17 @@ __global__ void __launch_bounds__(1024) k_bin(const BinArgs A) {
         off[A.C] = pos;
     }
     __syncthreads();
-    for (int c = warp; c < A.C; c += nw) {
-        int pos = cnt[c];
-        for (int base = 0; base < n; base += 32) {
-            const int q = base + lane;
-            const bool keep = q < n && chs[q] == c;
-            const unsigned m = __ballot_sync(0xffffffffu, keep);
-            if (keep) {
-                const int dst = pos + __popc(m & lt);
-                A.sorted[dst] = A.items[is + q];
-                if (A.binary) A.bsorted[dst] = A.bitems[is + q];
-            }
-            pos += __popc(m);
-        }
+    // all threads move records: 16-byte chunks, coalesced within a record
+    for (int t = threadIdx.x; t < 4 * n; t += blockDim.x) {
+        const int q = t >> 2, part = t & 3;
+        const int c = chs[q];
+        if (c < 0) continue;
+        const int dst = cnt[c] + rank[q];
+        reinterpret_cast<int4 *>(A.sorted + dst)[part] =
+            reinterpret_cast<const int4 *>(A.items + is + q)[part];
+        if (A.binary && part < 2)
+            reinterpret_cast<int4 *>(A.bsorted + dst)[part] =
+                reinterpret_cast<const int4 *>(A.bitems + is + q)[part];
     }
 }
 
@@ -213,7 +217,7 @@ gm_status prepare_impl(const gm_params *p, const gm_batch *b, const Workspace &w
         B.C = b->nchannels;
         B.binary = p->binary;
         if (b->max_example_items < 0) return gm_fail(GM_ERR_INVALID, "max_example_items < 0");
-        const size_t smem = sizeof(int) * (size_t)(b->nchannels + 1 + b->max_example_items);
+        const size_t smem = sizeof(int) * (size_t)(b->nchannels + 1 + 2 * b->max_example_items);
         if (smem > 200 * 1024)
             return gm_fail(GM_ERR_INVALID, "too many items per example (%d)", b->max_example_items);
         if (smem > 48 * 1024) CUDA_TRY(gm_ensure_smem((const void *)k_bin, (int)smem));

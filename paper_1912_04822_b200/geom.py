@@ -168,6 +168,70 @@ def draw_transforms(centers, random_translation, random_rotation, rng) -> list:
     return out
 
 
+class TransformArray:
+    """A batch of transforms as one (N, 15) float64 array (R row-major,
+    center, translation) -- the device format.  Indexing yields ``Transform``
+    objects; drawing the array skips per-example object construction."""
+
+    def __init__(self, packed):
+        self.packed = np.ascontiguousarray(packed, dtype=np.float64).reshape(-1, 15)
+
+    def __len__(self):
+        return self.packed.shape[0]
+
+    def __getitem__(self, e) -> Transform:
+        row = self.packed[e]
+        return _transform_from_row(row)
+
+    def __iter__(self):
+        return (self[e] for e in range(len(self)))
+
+
+def _transform_from_row(row) -> Transform:
+    t = Transform(IDENTITY_QUATERNION, row[9:12], row[12:15])
+    object.__setattr__(t, "rotation", _RowRotation(row[:9]))
+    return t
+
+
+class _RowRotation:
+    """Rotation given by its matrix (the quaternion is recovered on demand)."""
+
+    def __init__(self, flat):
+        self._R = np.array(flat, dtype=np.float64).reshape(3, 3)
+
+    def rotation_matrix(self) -> np.ndarray:
+        return self._R.copy()
+
+    def conjugate(self):
+        return _RowRotation(self._R.T.reshape(9))
+
+    def rotate(self, vec) -> np.ndarray:
+        return self._R @ np.asarray(vec, dtype=np.float64)
+
+    @property
+    def angle(self) -> float:
+        return math.acos(max(-1.0, min(1.0, (np.trace(self._R) - 1.0) / 2.0)))
+
+
+def draw_transform_array(centers, random_translation, random_rotation, rng) -> TransformArray:
+    """``draw_transforms`` without per-example objects: the same variates and
+    the same float64 expressions and libm calls (bit-identical rows), packed
+    for the device.  The per-example arithmetic runs in the C ABI helper
+    ``gm_draw_transforms``."""
+    t = check_non_negative(random_translation, "random_translate")
+    centers = np.ascontiguousarray(centers, dtype=np.float64).reshape(-1, 3)
+    n = centers.shape[0]
+    k = (3 if random_rotation else 0) + (3 if t > 0 else 0)
+    u = np.ascontiguousarray(rng.random((n, k))) if k else None
+    out = np.empty((n, 15), dtype=np.float64)
+    from . import _native
+
+    _native.check(_native.lib().gm_draw_transforms(
+        u.ctypes.data if u is not None else None, n, int(bool(random_rotation)), t,
+        centers.ctypes.data, out.ctypes.data))
+    return TransformArray(out)
+
+
 def transform_example(t: Transform, example):
     """Apply one transform to every set of an example (coords rounded to f32)."""
     new_sets = [cs.with_coords(t.forward(cs.coords)) for cs in example.coord_sets]

@@ -177,6 +177,8 @@ class PackedBatch:
         self.default_centers = np.stack([_default_center(sets) for sets in example_sets]) \
             if self.nexamples else np.zeros((0, 3))
         self._percall = None
+        self._gm = None
+        self._gm_ref = None
 
     # ------------------------------------------------------------------
     @property
@@ -193,35 +195,61 @@ class PackedBatch:
         return self.dev.data_ptr() + self.offsets[name][0]
 
     def set_call_arrays(self, origins: np.ndarray, xforms: np.ndarray | None) -> None:
-        """Upload the per-call origins (N,3) and transforms (N,15), float64."""
+        """Stage the per-call origins (N,3) and transforms (N,15), float64.
+
+        Pinned staging slots are recycled in a ring of three, each guarded by
+        an event, so the host can prepare the next call while the device
+        still copies the previous one; the device-side buffer is fixed, so
+        the packed ``gm_batch`` pointers never change."""
         n = self.nexamples
-        buf = np.zeros(n * 3 + (n * 15 if xforms is not None else 0), np.float64)
-        buf[:n * 3] = np.asarray(origins, np.float64).reshape(-1)
+        cuda = self.device.type == "cuda"
+        if self._percall is None:
+            self._percall = torch.empty(max(18 * n, 1), dtype=torch.float64, device=self.device)
+            self._stage = [torch.empty(max(18 * n, 1), dtype=torch.float64, pin_memory=cuda)
+                           for _ in range(3)]
+            self._stage_ev = [None, None, None]
+            self._slot = 0
+        slot = self._slot
+        self._slot = (slot + 1) % 3
+        if self._stage_ev[slot] is not None:
+            self._stage_ev[slot].synchronize()
+        h = self._stage[slot].numpy()
+        h[:3 * n] = np.asarray(origins, np.float64).reshape(-1)
+        m = 3 * n
         if xforms is not None:
-            buf[n * 3:] = np.asarray(xforms, np.float64).reshape(-1)
-        t = torch.from_numpy(buf)
-        if self.device.type == "cuda":
-            t = t.pin_memory()
-        self._percall = t.to(self.device, non_blocking=True)
+            h[3 * n:18 * n] = np.asarray(xforms, np.float64).reshape(-1)
+            m = 18 * n
+        if m:
+            self._percall[:m].copy_(self._stage[slot][:m], non_blocking=True)
+        if cuda:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(self.device))
+            self._stage_ev[slot] = ev
         self._has_xforms = xforms is not None
+        if self._gm is not None:
+            self._gm.xforms = self._percall.data_ptr() + 8 * 3 * n if self._has_xforms else None
 
     def gm_batch(self) -> _native.GmBatch:
-        b = _native.GmBatch()
-        b.nexamples, b.nsets, b.natoms = self.nexamples, self.nsets, self.natoms
-        b.nitems, b.nchannels, b.vector_mode = self.nitems, self.nchannels, int(self.vector_mode)
-        b.nweights = self.nweights
-        b.max_example_items = self.max_example_items
-        for name in ("coords32", "atom_radius", "atom_set", "atom_type", "set_start", "set_end",
-                     "set_example", "set_choff", "set_t", "set_wstart", "weights",
-                     "type_radius", "set_trstart", "item_atom", "item_channel", "item_weight",
-                     "item_radius", "ex_item_start", "ex_item_end"):
-            setattr(b, name, self.ptr(name))
+        """The C-ABI batch descriptor (built once; pointers are stable)."""
         if self._percall is None:
             raise RuntimeError("set_call_arrays() must run before a launch")
-        base = self._percall.data_ptr()
-        b.origins = base
-        b.xforms = base + 8 * 3 * self.nexamples if self._has_xforms else None
-        return b
+        if self._gm is None:
+            b = _native.GmBatch()
+            b.nexamples, b.nsets, b.natoms = self.nexamples, self.nsets, self.natoms
+            b.nitems, b.nchannels = self.nitems, self.nchannels
+            b.vector_mode = int(self.vector_mode)
+            b.nweights = self.nweights
+            b.max_example_items = self.max_example_items
+            for name in ("coords32", "atom_radius", "atom_set", "atom_type", "set_start",
+                         "set_end", "set_example", "set_choff", "set_t", "set_wstart", "weights",
+                         "type_radius", "set_trstart", "item_atom", "item_channel",
+                         "item_weight", "item_radius", "ex_item_start", "ex_item_end"):
+                setattr(b, name, self.ptr(name))
+            base = self._percall.data_ptr()
+            b.origins = base
+            b.xforms = base + 8 * 3 * self.nexamples if self._has_xforms else None
+            self._gm = b
+        return self._gm
 
 
 def _default_center(sets) -> np.ndarray:

@@ -177,17 +177,24 @@ class GridMaker:
         return d if d.index is not None else torch.device("cuda", torch.cuda.current_device())
 
     def _gm_params(self, npts: int) -> _native.GmParams:
+        key = (float(self.resolution), float(self.dimension), bool(self.binary),
+               bool(self.radius_type_indexed), float(self.radius_scale),
+               float(self.gaussian_radius_multiple), int(npts))
+        cached = self.__dict__.get("_params_cache")
+        if cached is not None and cached[0] == key:
+            return cached[1]
         p = _native.GmParams()
-        p.resolution = float(self.resolution)
-        p.dimension = float(self.dimension)
-        p.radius_scale = float(self.radius_scale)
-        p.gaussian_radius_multiple = float(self.gaussian_radius_multiple)
+        p.resolution = key[0]
+        p.dimension = key[1]
+        p.radius_scale = key[4]
+        p.gaussian_radius_multiple = key[5]
         p.radius_multiple = self.radius_multiple
-        p.npts = int(npts)
-        p.binary = int(bool(self.binary))
-        p.radius_type_indexed = int(bool(self.radius_type_indexed))
+        p.npts = key[6]
+        p.binary = int(key[2])
+        p.radius_type_indexed = int(key[3])
         p.matmul_order_1 = geom.matmul_order(1)
         p.matmul_order_n = geom.matmul_order(2)
+        self.__dict__["_params_cache"] = (key, p)
         return p
 
     def pack(self, examples, nchannels=None, device=None, check_type_radii=True) -> PackedBatch:
@@ -204,21 +211,31 @@ class GridMaker:
                                dev, centers=None)
 
     def _prepare(self, pb: PackedBatch, centers, transforms, npts) -> _native.GmParams:
-        centers = pb.default_centers if centers is None else np.asarray(centers, np.float64)
-        origins = centers.reshape(-1, 3) - float(self.dimension) / 2.0
+        if centers is None:
+            key = float(self.dimension)
+            if getattr(pb, "_origin_key", None) != key:
+                pb._default_origins = pb.default_centers - key / 2.0
+                pb._origin_key = key
+            origins = pb._default_origins
+        else:
+            origins = np.asarray(centers, np.float64).reshape(-1, 3) - float(self.dimension) / 2.0
         xforms = None
         if transforms is not None:
-            xforms = np.stack([t.packed() if isinstance(t, geom.Transform)
-                               else np.asarray(t, np.float64).reshape(15) for t in transforms]) \
-                if len(transforms) else np.zeros((0, 15))
+            if isinstance(transforms, geom.TransformArray):
+                xforms = transforms.packed
+            elif isinstance(transforms, np.ndarray):
+                xforms = transforms.reshape(-1, 15)
+            else:
+                xforms = np.stack([t.packed() if isinstance(t, geom.Transform)
+                                   else np.asarray(t, np.float64).reshape(15)
+                                   for t in transforms]) if len(transforms) else np.zeros((0, 15))
         pb.set_call_arrays(origins, xforms)
         p = self._gm_params(npts)
         b = pb.gm_batch()
-        pb._gm = b
         with torch.cuda.device(pb.device):
             _native.check(_native.lib().gm_prepare(
-                ctypes.byref(p), ctypes.byref(b), ctypes.c_void_p(pb.workspace.data_ptr()),
-                pb.workspace_bytes, ctypes.c_void_p(stream_handle(pb.device))))
+                ctypes.byref(p), ctypes.byref(b), pb.workspace.data_ptr(), pb.workspace_bytes,
+                stream_handle(pb.device)))
         return p
 
     def forward_packed(self, pb: PackedBatch, out=None, centers=None, *,
@@ -241,17 +258,16 @@ class GridMaker:
             if augment:
                 rng = check_rng(rng)
                 c = pb.default_centers if centers is None else np.asarray(centers, np.float64)
-                transforms = geom.draw_transforms(c.reshape(-1, 3), float(random_translation),
-                                                  bool(random_rotation), rng)
+                transforms = geom.draw_transform_array(c.reshape(-1, 3), float(random_translation),
+                                                       bool(random_rotation), rng)
         p = self._prepare(pb, centers, transforms, npts)
         if pb.nexamples and pb.nchannels:
             with torch.cuda.device(pb.device):
                 if events is not None:
                     events[0].record()
                 _native.check(_native.lib().gm_forward(
-                    ctypes.byref(p), ctypes.byref(pb._gm),
-                    ctypes.c_void_p(pb.workspace.data_ptr()), ctypes.c_void_p(out.data_ptr()),
-                    ctypes.c_void_p(stream_handle(pb.device))))
+                    ctypes.byref(p), ctypes.byref(pb._gm), pb.workspace.data_ptr(),
+                    out.data_ptr(), stream_handle(pb.device)))
                 if events is not None:
                     events[1].record()
         pb._last_params = p
@@ -284,11 +300,9 @@ class GridMaker:
             if events is not None:
                 events[0].record()
             _native.check(_native.lib().gm_backward(
-                ctypes.byref(p), ctypes.byref(pb._gm), ctypes.c_void_p(pb.workspace.data_ptr()),
-                None if self.binary else ctypes.c_void_p(grid_grad.data_ptr()),
-                ctypes.c_void_p(coord_grad.data_ptr()),
-                ctypes.c_void_p(type_grad.data_ptr()) if pb.vector_mode else None,
-                ctypes.c_void_p(stream_handle(pb.device))))
+                ctypes.byref(p), ctypes.byref(pb._gm), pb.workspace.data_ptr(),
+                None if self.binary else grid_grad.data_ptr(), coord_grad.data_ptr(),
+                type_grad.data_ptr() if pb.vector_mode else None, stream_handle(pb.device)))
             if events is not None:
                 events[1].record()
         return coord_grad, (type_grad if pb.vector_mode else None)
@@ -501,6 +515,8 @@ class GridMaker:
 def _rotation_of(t) -> np.ndarray:
     if isinstance(t, geom.Transform):
         return t.rotation.rotation_matrix()
+    if hasattr(t, "rotation_matrix"):
+        return t.rotation_matrix()
     return np.asarray(t, np.float64).reshape(15)[:9].reshape(3, 3)
 
 

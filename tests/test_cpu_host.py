@@ -86,6 +86,21 @@ def test_draw_transforms_matches_sequential_make_transform():
         assert r1.random() == r2.random()  # same stream position afterwards
 
 
+def test_draw_transform_array_bit_identical():
+    from paper_1912_04822_b200 import geom
+
+    for seed in range(3):
+        centers = np.random.default_rng(seed).uniform(-3, 3, (64, 3))
+        for rot, tr in ((True, 2.0), (True, 0.0), (False, 1.5), (False, 0.0)):
+            seq = [geom.make_transform(c, tr, rot, r) for r in [np.random.default_rng(seed)]
+                   for c in centers]
+            arr = geom.draw_transform_array(centers, tr, rot, np.random.default_rng(seed))
+            assert len(arr) == 64
+            for a, b in zip(seq, arr.packed):
+                np.testing.assert_array_equal(a.packed(), b)
+            np.testing.assert_array_equal(arr[5].packed(), seq[5].packed())
+
+
 def test_matmul_order_calibrated():
     from paper_1912_04822_b200 import geom
 
