@@ -177,51 +177,134 @@ __device__ __forceinline__ void store_coord(const BwdArgs &P, int a, int lane, d
     }
 }
 
-__global__ void __launch_bounds__(256, 3) k_backward_index(const BwdArgs P) {
-    __shared__ Tables tabs[kWarps];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int a = blockIdx.x * kWarps + warp;
+// ---------------------------------------------------------------------------
+// Index types: kLPA lanes per atom.  The lanes of an atom share per-axis
+// tables (offset, f64 Gaussian factor; kSub entries per axis, sub-boxes for
+// larger boxes) and split its (i, j) rows round-robin; each row walks only
+// its k span inside the cutoff sphere, two voxels at a time, branch-free
+// (voxels outside the sphere load nothing and add an exact 0).
+// ---------------------------------------------------------------------------
+constexpr int kLPA = 4;                 // lanes per atom
+constexpr int kSub = 16;                // table entries per axis
+constexpr int kAtomsPerBlock = 256 / kLPA;
+
+struct SmallTables {
+    double dx[kSub], ex[kSub], dy[kSub], ey[kSub], dz[kSub], ez[kSub];
+};
+
+__global__ void __launch_bounds__(256, 2) k_backward_index(const BwdArgs P) {
+    __shared__ SmallTables tabs[kAtomsPerBlock];
+    const int sub = threadIdx.x & (kLPA - 1);
+    const int slot = threadIdx.x / kLPA;
+    const int a = blockIdx.x * kAtomsPerBlock + slot;
     const gm_batch &b = P.b;
-    if (a >= b.natoms) return;
+    const bool live = a < b.natoms;
     const int D = P.p.npts;
     const double res = P.p.resolution, grm = P.p.gaussian_radius_multiple;
     const float inv_res = (float)(1.0 / res);
-    Atom A;
-    int s, e;
-    load_atom(P, a, A, s, e);
-    const int c = b.set_choff[s] + b.atom_type[a];
-    const double r = b.atom_radius[a];
-    const double d0 = grm * r, d02 = d0 * d0;
-    const double q0 = (2.0 * grm) / r;
-    const double qa2 = 2.0 * (exp((-2.0 * grm) * grm) * (q0 * q0));
-    const double m4inv_r2 = -4.0 / (r * r);
+    SmallTables &T = tabs[slot];
+    // the lanes of one atom (they share T); atoms of a warp may run different
+    // sub-box loops, so synchronise only the group
+    const unsigned gmask = ((1u << kLPA) - 1u) << ((threadIdx.x & 31) & ~(kLPA - 1));
     double ax0 = 0.0, ay0 = 0.0, az0 = 0.0, ax1 = 0.0, ay1 = 0.0, az1 = 0.0;
-    if (set_radius(A, r, P.p.radius_multiple, res, D)) {
-        const double dzr = A.dzr;
-        const float *gbase = P.grid_grad + ((size_t)e * b.nchannels + c) * ((size_t)D * D * D);
-        walk<true, true>(A, tabs[warp], gbase, D, res, inv_res, lane,
-                         [&](int slot, double d2, double dx, double dy, double dz, double exyz,
-                             double g) {
-                             // slope/d: Gaussian exp(-2d^2/r^2)(-4/r^2); tail 2qa(d - dzr)/d
-                             double sc;
-                             if (d2 <= d02) {
-                                 sc = g * exyz * m4inv_r2;
-                             } else {
-                                 const double rd = rsqrt_d(d2);
-                                 sc = g * (qa2 * fma(d2, rd, -dzr)) * rd;
-                             }
-                             if (slot) {
-                                 ax1 = fma(sc, dx, ax1);
-                                 ay1 = fma(sc, dy, ay1);
-                                 az1 = fma(sc, dz, az1);
-                             } else {
-                                 ax0 = fma(sc, dx, ax0);
-                                 ay0 = fma(sc, dy, ay0);
-                                 az0 = fma(sc, dz, az0);
-                             }
-                         });
+    Atom A;
+    bool any = false;
+    int e = 0, c = 0;
+    double d02 = 0.0, qa2 = 0.0, m4inv_r2 = 0.0;
+    if (live) {
+        int s;
+        load_atom(P, a, A, s, e);
+        c = b.set_choff[s] + b.atom_type[a];
+        const double r = b.atom_radius[a];
+        const double d0 = grm * r;
+        d02 = d0 * d0;
+        const double q0 = (2.0 * grm) / r;
+        qa2 = 2.0 * (exp((-2.0 * grm) * grm) * (q0 * q0));
+        m4inv_r2 = -4.0 / (r * r);
+        any = set_radius(A, r, P.p.radius_multiple, res, D);
     }
-    store_coord(P, a, lane, ax0 + ax1, ay0 + ay1, az0 + az1);
+    const size_t D3 = (size_t)D * D * D;
+    const float *gbase = P.grid_grad + ((size_t)e * b.nchannels + c) * D3;
+    // sub-box loop bounds are uniform across the atom's lanes
+    const int si_end = any ? A.i1 : -1;
+    for (int si = any ? A.i0 : 0; si <= si_end; si += kSub)
+        for (int sj = A.j0; sj <= A.j1; sj += kSub)
+            for (int sk = A.k0; sk <= A.k1; sk += kSub) {
+                const int ni = min(kSub, A.i1 - si + 1), nj = min(kSub, A.j1 - sj + 1),
+                          nk = min(kSub, A.k1 - sk + 1);
+                __syncwarp(gmask);
+                for (int l = sub; l < 3 * kSub; l += kLPA) {
+                    const int ax = l / kSub, q = l - ax * kSub;
+                    const int n = ax == 0 ? ni : (ax == 1 ? nj : nk);
+                    if (q < n) {
+                        const double x = ax == 0 ? A.x : (ax == 1 ? A.y : A.z);
+                        const double o = ax == 0 ? A.ox : (ax == 1 ? A.oy : A.oz);
+                        const int i0 = ax == 0 ? si : (ax == 1 ? sj : sk);
+                        const double d = offs(x, o, i0 + q, res);
+                        const double E = exp(A.m2inv_r2 * (d * d));
+                        double *dt = ax == 0 ? T.dx : (ax == 1 ? T.dy : T.dz);
+                        double *et = ax == 0 ? T.ex : (ax == 1 ? T.ey : T.ez);
+                        dt[q] = d;
+                        et[q] = E;
+                    }
+                }
+                __syncwarp(gmask);
+                const float inv_nj = __frcp_rn((float)nj);
+                const float dz0 = (float)T.dz[0];
+                const float *gsub = gbase + ((size_t)si * D + sj) * D + sk;
+                for (int row = sub; row < ni * nj; row += kLPA) {
+                    const int ii = idiv(row, inv_nj), jj = row - ii * nj;
+                    const double dx = T.dx[ii], dy = T.dy[jj];
+                    const double b2 = fma(dy, dy, dx * dx);
+                    const double rem = A.dzr2 - b2;
+                    if (rem <= 0.0) continue;
+                    const float rho = fmaf(sqrtf((float)rem), 1.0001f, 1e-5f * (float)A.dzr);
+                    const int klo = max(0, (int)ceilf(fmaxf((dz0 - rho) * inv_res, -1.0f)));
+                    const int khi =
+                        min(nk - 1, (int)floorf(fminf((dz0 + rho) * inv_res, (float)nk)));
+                    const double exy = T.ex[ii] * T.ey[jj] * m4inv_r2;
+                    const float *gr = gsub + ((size_t)ii * D + jj) * D;
+                    // the whole row span first (<= kSub loads in flight), then the math
+                    float g[kSub];
+#pragma unroll
+                    for (int q = 0; q < kSub; q++)
+                        g[q] = (klo + q <= khi) ? __ldg(gr + klo + q) : 0.0f;
+#pragma unroll
+                    for (int q = 0; q < kSub; q++) {
+                        if (klo + q > khi) break;
+                        const int kk = klo + q;
+                        const double dz = T.dz[kk];
+                        const double d2 = fma(dz, dz, b2);
+                        const bool in = d2 > 0.0 && d2 < A.dzr2;
+                        const double gv = in ? (double)g[q] : 0.0;
+                        const double rd = rsqrt_d(d2);
+                        const double sq = gv * (qa2 * fma(d2, rd, -A.dzr)) * rd;
+                        const double sg = gv * (exy * T.ez[kk]);
+                        const double sc = d2 <= d02 ? sg : sq;
+                        if (q & 1) {
+                            ax1 = fma(sc, dx, ax1);
+                            ay1 = fma(sc, dy, ay1);
+                            az1 = fma(sc, dz, az1);
+                        } else {
+                            ax0 = fma(sc, dx, ax0);
+                            ay0 = fma(sc, dy, ay0);
+                            az0 = fma(sc, dz, az0);
+                        }
+                    }
+                }
+            }
+    double gx = ax0 + ax1, gy = ay0 + ay1, gz = az0 + az1;
+#pragma unroll
+    for (int o = 1; o < kLPA; o <<= 1) {
+        gx += __shfl_xor_sync(0xffffffffu, gx, o);
+        gy += __shfl_xor_sync(0xffffffffu, gy, o);
+        gz += __shfl_xor_sync(0xffffffffu, gz, o);
+    }
+    if (live && sub == 0) {
+        P.coord_grad[3 * a + 0] = (float)gx;
+        P.coord_grad[3 * a + 1] = (float)gy;
+        P.coord_grad[3 * a + 2] = (float)gz;
+    }
 }
 
 // Vector types (_kernels.py:258-314).  With per-atom radii and <= kMaxT
@@ -353,9 +436,10 @@ gm_status backward_impl(const gm_params *p, const gm_batch *b, const Workspace &
     P.grid_grad = grid_grad;
     P.coord_grad = coord_grad;
     P.type_grad = type_grad;
-    const int blocks = (b->natoms + kWarps - 1) / kWarps;
-    if (b->vector_mode) k_backward_vector<<<blocks, 256, 0, s>>>(P);
-    else k_backward_index<<<blocks, 256, 0, s>>>(P);
+    if (b->vector_mode)
+        k_backward_vector<<<(b->natoms + kWarps - 1) / kWarps, 256, 0, s>>>(P);
+    else
+        k_backward_index<<<(b->natoms + kAtomsPerBlock - 1) / kAtomsPerBlock, 256, 0, s>>>(P);
     LAUNCH_CHECK();
     return GM_OK;
 }
