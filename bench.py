@@ -63,59 +63,65 @@ def load_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled by NVML in a background thread
+    while the timed region runs (nvidia-smi's 100 ms minimum interval is
+    longer than a short timed region)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.thread = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except Exception:
-            self.proc = None
+            import pynvml
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = self.index
+            if vis:
+                try:
+                    idx = int(vis.split(",")[self.index])
+                except ValueError:
+                    idx = self.index
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.nvml = pynvml
+        except Exception:
+            self.h = None
+            return
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+
+    def _run(self):
+        nv = self.nvml
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for b, name in self.REASONS.items():
+                    if bits & b:
+                        self.reasons.add(name)
+            except Exception:
+                break
+            time.sleep(0.002)
 
     def stop(self):
-        if self.proc is None:
+        if self.thread is None:
             return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
+        self._stop.set()
         self.thread.join(timeout=2)
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
+        if not self.samples:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
 def dist_env():
@@ -125,18 +131,17 @@ def dist_env():
     return ws, rank, local
 
 
-def make_batch(cfg, rank, n=None):
-    from paper_1912_04822_b200 import synthetic
+def make_batch(cfg, rank, world=1, n=None):
+    """This rank's examples of the global batch (world * B examples drawn in
+    order from one stream; rank r takes [r*B, (r+1)*B)), and
+    the default centers of the whole global batch (for the transform draw)."""
+    from paper_1912_04822_b200 import distributed, synthetic
 
     n = cfg["batch"] if n is None else n
-    # rank r grids examples [r*B, (r+1)*B) of one global stream
     rng = np.random.default_rng(cfg["seed"])
-    exs = []
-    for i in range((rank + 1) * n):
-        ex = synthetic.complex_example(rng, vector=cfg["vector"])
-        if i >= rank * n:
-            exs.append(ex)
-    return exs
+    glob = [synthetic.complex_example(rng, vector=cfg["vector"]) for _ in range(world * n)]
+    centers = np.stack([ex.coord_sets[-1].centroid() for ex in glob])
+    return distributed.shard(glob, rank, world), centers
 
 
 def bytes_model(cfg, exs, footprint):
@@ -193,7 +198,7 @@ def run_reference(args, cfg):
     ws, rank, local = dist_env()
     if rank != 0:
         return 0
-    exs = make_batch(cfg, 0, n=8)
+    exs, _ = make_batch(cfg, 0, n=8)
     import oracle
 
     oracle.build()
@@ -255,9 +260,9 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
-    from paper_1912_04822_b200 import GridMaker, _native
+    from paper_1912_04822_b200 import GridMaker, _native, distributed, geom
 
-    exs = make_batch(cfg, rank)
+    exs, global_centers = make_batch(cfg, rank, ws)
     gm = GridMaker(resolution=cfg["resolution"], dimension=cfg["dimension"],
                    binary=cfg["binary"], device=dev)
     D = gm.points_per_side()
@@ -268,14 +273,18 @@ def main():
                      device=dev, dtype=torch.float32)
     cg = torch.empty((pb.natoms, 3), dtype=torch.float32, device=dev)
     tg = torch.empty((max(pb.nweights, 1),), dtype=torch.float32, device=dev) if pb.vector_mode else None
-    rng = np.random.default_rng(1234 + rank)
+    rng = np.random.default_rng(1234)  # same stream on every rank
     stream = torch.cuda.current_stream(dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
+    def draw():
+        # transforms of the whole global batch in example order, this rank's slice
+        full = geom.draw_transform_array(global_centers, 2.0, True, rng)
+        return distributed.shard_transforms(full, rank, ws)
+
     def step(fwd_ev=None, bwd_ev=None):
         # events bracket exactly the k_forward / k_backward launches
-        gm.forward_packed(pb, out, random_rotation=True, random_translation=2.0, rng=rng,
-                          events=fwd_ev)
+        gm.forward_packed(pb, out, transforms=draw(), events=fwd_ev)
         gm.backward_packed(pb, gg, reuse_prepared=True, coord_grad=cg, type_grad=tg,
                            events=bwd_ev)
 
@@ -324,7 +333,7 @@ def main():
 
         def e2e_step():
             pb.upload()  # H2D of the packed atoms (pinned)
-            gm.forward_packed(pb, out, random_rotation=True, random_translation=2.0, rng=rng)
+            gm.forward_packed(pb, out, transforms=draw())
             gm.backward_packed(pb, out, reuse_prepared=True, coord_grad=cg, type_grad=tg)
             host_cg.copy_(cg, non_blocking=True)
 

@@ -235,69 +235,78 @@ class GridOracle:
         self.forward_placed(out, placed, origins)
         return out
 
-    def forward_placed(self, out, placed, origins):
-        """voxelizer.py:372-435: pack CSR arrays and dispatch to the C kernels."""
+    def pack_placed(self, placed):
+        """voxelizer.py:372-435: the packed CSR arrays of the reference's
+        _kernels calls, as a dict (keys = _kernels argument names)."""
         nonempty = [p for p in placed if p[2].coords.shape[0]]
-        if not nonempty:
-            return out
-        vector_mode = nonempty[0][2].type_vector is not None
+        vector_mode = bool(nonempty) and nonempty[0][2].type_vector is not None
         nsets = len(placed)
         natoms = sum(p[2].coords.shape[0] for p in placed)
-        coords_all = np.zeros((natoms, 3), dtype=np.float64)
-        set_start = np.zeros(nsets, np.int64)
-        set_end = np.zeros(nsets, np.int64)
-        set_example = np.zeros(nsets, np.int64)
-        set_choff = np.zeros(nsets, np.int64)
-        set_t = np.zeros(nsets, np.int64)
+        d = dict(coords=np.zeros((natoms, 3), dtype=np.float64),
+                 set_start=np.zeros(nsets, np.int64), set_end=np.zeros(nsets, np.int64),
+                 set_example=np.zeros(nsets, np.int64), set_choff=np.zeros(nsets, np.int64),
+                 set_t=np.zeros(nsets, np.int64), vector_mode=vector_mode)
         pos = 0
         for s, (e, choff, cs, c64) in enumerate(placed):
             na = cs.coords.shape[0]
-            set_start[s], set_end[s] = pos, pos + na
-            set_example[s], set_choff[s], set_t[s] = e, choff, cs.num_types
-            coords_all[pos:pos + na] = c64
+            d["set_start"][s], d["set_end"][s] = pos, pos + na
+            d["set_example"][s], d["set_choff"][s], d["set_t"][s] = e, choff, cs.num_types
+            d["coords"][pos:pos + na] = c64
             pos += na
         scale = self.radius_scale
-        L = lib()
-        origins = np.ascontiguousarray(origins, dtype=np.float64)
-        D = out.shape[2]
         if vector_mode:
             wtot = sum(p[2].coords.shape[0] * p[2].num_types for p in placed)
-            weights_flat = np.zeros(wtot, np.float64)
-            w_start = np.zeros(nsets, np.int64)
-            tr_flat = np.zeros(max(1, sum(p[2].num_types for p in placed)), np.float64)
-            tr_start = np.zeros(nsets, np.int64)
-            atom_radii = np.zeros(natoms, np.float64)
+            d["weights_flat"] = np.zeros(wtot, np.float64)
+            d["w_start"] = np.zeros(nsets, np.int64)
+            d["type_radii_flat"] = np.zeros(max(1, sum(p[2].num_types for p in placed)),
+                                            np.float64)
+            d["tr_start"] = np.zeros(nsets, np.int64)
+            d["atom_radii"] = np.zeros(natoms, np.float64)
             wpos = tpos = 0
             for s, (e, choff, cs, c64) in enumerate(placed):
                 na, nt = cs.coords.shape[0], cs.num_types
-                w_start[s] = wpos
+                d["w_start"][s] = wpos
                 if na:
-                    weights_flat[wpos:wpos + na * nt] = cs.type_vector.astype(np.float64).ravel()
+                    d["weights_flat"][wpos:wpos + na * nt] = \
+                        cs.type_vector.astype(np.float64).ravel()
                 wpos += na * nt
-                tr_start[s] = tpos
+                d["tr_start"][s] = tpos
                 if na and self.radius_type_indexed:
-                    tr_flat[tpos:tpos + nt] = cs.type_radii.astype(np.float64) * scale
+                    d["type_radii_flat"][tpos:tpos + nt] = cs.type_radii.astype(np.float64) * scale
                 else:
-                    tr_flat[tpos:tpos + nt] = 1.0
+                    d["type_radii_flat"][tpos:tpos + nt] = 1.0
                 tpos += nt
-                atom_radii[set_start[s]:set_end[s]] = cs.radii.astype(np.float64) * scale
-            L.oracle_forward_vector_sets(
-                out, out.shape[1], D, coords_all, weights_flat, w_start, atom_radii,
-                tr_flat, tr_start, int(self.radius_type_indexed), set_start, set_end,
-                set_example, set_choff, set_t, nsets, origins, self.resolution, self.grm,
-                self.rmult, int(self.binary))
+                d["atom_radii"][d["set_start"][s]:d["set_end"][s]] = \
+                    cs.radii.astype(np.float64) * scale
         else:
-            radii_all = np.zeros(natoms, np.float64)
-            tidx_all = np.zeros(natoms, np.int64)
+            d["radii"] = np.zeros(natoms, np.float64)
+            d["tidx"] = np.zeros(natoms, np.int64)
             for s, (e, choff, cs, c64) in enumerate(placed):
                 if cs.coords.shape[0] == 0:
                     continue
-                radii_all[set_start[s]:set_end[s]] = cs.radii.astype(np.float64) * scale
-                tidx_all[set_start[s]:set_end[s]] = cs.type_index
+                d["radii"][d["set_start"][s]:d["set_end"][s]] = cs.radii.astype(np.float64) * scale
+                d["tidx"][d["set_start"][s]:d["set_end"][s]] = cs.type_index
+        return d
+
+    def forward_placed(self, out, placed, origins):
+        """voxelizer.py:372-435: pack CSR arrays and dispatch to the C kernels."""
+        if not any(p[2].coords.shape[0] for p in placed):
+            return out
+        d = self.pack_placed(placed)
+        L = lib()
+        origins = np.ascontiguousarray(origins, dtype=np.float64)
+        D = out.shape[2]
+        sets = (d["set_start"], d["set_end"], d["set_example"], d["set_choff"], d["set_t"])
+        if d["vector_mode"]:
+            L.oracle_forward_vector_sets(
+                out, out.shape[1], D, d["coords"], d["weights_flat"], d["w_start"],
+                d["atom_radii"], d["type_radii_flat"], d["tr_start"],
+                int(self.radius_type_indexed), *sets, len(placed), origins, self.resolution,
+                self.grm, self.rmult, int(self.binary))
+        else:
             L.oracle_forward_index_sets(
-                out, out.shape[1], D, coords_all, radii_all, tidx_all, set_start, set_end,
-                set_example, set_choff, set_t, nsets, origins, self.resolution, self.grm,
-                self.rmult, int(self.binary))
+                out, out.shape[1], D, d["coords"], d["radii"], d["tidx"], *sets, len(placed),
+                origins, self.resolution, self.grm, self.rmult, int(self.binary))
         return out
 
     def forward(self, cs, center=None, random_translation=0.0, random_rotation=False, rng=None):
