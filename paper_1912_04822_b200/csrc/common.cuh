@@ -72,6 +72,7 @@ struct Workspace {
     int32_t *item_ch;    // nitems: channel, or -1 when the box misses the grid
     FwdItem *sorted;     // nitems: per example, grouped by channel in item order
     BinItem *bsorted;    // nitems (binary mode)
+    int2 *sbox;          // nitems: {ibox, jbox} of sorted items (forward culling)
     int32_t *chan_off;   // nexamples * (nchannels + 1): ranges into sorted
 };
 
@@ -95,6 +96,7 @@ inline size_t carve_workspace(void *base, int32_t natoms, int32_t nitems, int32_
     ws->item_ch = (int32_t *)take(sizeof(int32_t) * ni);
     ws->sorted = (FwdItem *)take(sizeof(FwdItem) * ni);
     ws->bsorted = (BinItem *)take(sizeof(BinItem) * ni);
+    ws->sbox = (int2 *)take(sizeof(int2) * ni);
     ws->chan_off = (int32_t *)take(sizeof(int32_t) * (size_t)std::max(nex, 1) * (nch + 1));
     return off + 256;
 }

@@ -5,30 +5,32 @@
 // density over its integer voxel box, rounded once to f32.
 //
 // Work decomposition (B200): one CTA per (example, channel, tile of TI planes
-// x TJ rows x all D columns).  The tile accumulates in shared memory (dense
-// [TI][TJ][D], <= 80 KB, 2 CTAs/SM).  The CTA reads only its channel's items
-// (k_bin grouped them), keeps those whose box meets the tile (ordered ballot
-// compaction into a shared list) and hands every warp a disjoint region of the
-// tile (one plane, or a band of rows of one plane).  A warp walks the list in
-// order and scatters each item's box cross-section into its region: lane ->
-// (row offset, column) with the column fixed per item, so per voxel the work is
-// one FMA for the row coordinate, d^2, exp2, rsqrt for the tail and a
-// shared-memory accumulate.  Regions are disjoint and each warp adds items in
-// order, so every voxel is summed in the reference's item order without
-// atomics.  The finished tile (zeros included) is written with TMA bulk
-// stores (cp.async.bulk) when D % 4 == 0: planes of the tile are contiguous in
-// global memory.  CTAs whose channel has no items only stream zeros.
+// x TJ rows x all D columns); the tile accumulates in shared memory (dense
+// [TI][TJ][D]).  Each warp owns a disjoint region of the tile (one plane, or a
+// band of rows of one plane) and walks the channel's items (k_bin grouped them
+// by channel, in item order) 32 at a time:
+//   phase A (lane t <-> item t): box test against the region, the sphere's
+//           cross-section with the plane (row / column spans, ~2/3 of the box
+//           face), per-visit constants -> a per-warp shared-memory slot;
+//   phase B (items in order): every lane reads the slot (broadcast) and
+//           scatters its (row, column) voxels: one FMA per row coordinate,
+//           d^2, ex2 (Gaussian core), sqrt (tail), a shared-memory accumulate.
+// Regions are disjoint and each warp adds its items in order, so every voxel
+// is summed in the reference's item order without atomics.  The finished tile
+// (zeros included) leaves through TMA bulk stores (cp.async.bulk) when
+// D % 4 == 0: the planes of a tile are contiguous in global memory.  CTAs
+// whose channel has no item only stream zeros.
 #include "common.cuh"
 
 namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kCap = 384;  // shared item-list capacity per round
 
 struct FwdArgs {
     const FwdItem *sorted;
     const BinItem *bsorted;
+    const int2 *sbox;
     const int32_t *chan_off;
     const double *origins;
     float *out;
@@ -38,6 +40,19 @@ struct FwdArgs {
     int bulk;
     size_t acc_floats;
 };
+
+// Per-visit constants of one item for one warp region (phase A -> phase B).
+struct __align__(16) Slot {
+    float yh, yl, zh, zl;      // row / column offsets at the box corner (hi, lo)
+    float dx2, cexp, d02, cut; // plane offset^2, -2 log2(e)/r^2, (grm r)^2, cutoff
+    float qa, w;               // quadratic coefficient, weight
+    int jspan, kspan;          // first row / column relative to the box corner | count << 16
+    int arow;                  // accumulator offset of (first row, box column 0)
+    int rpi;                   // rows per pass = 32 / min(32, columns)
+    int src;                   // item index (binary mode re-reads the f64 record)
+    int pad;
+};
+static_assert(sizeof(Slot) == 64, "Slot must be 64 bytes");
 
 __device__ __forceinline__ void bulk_store(float *gdst, const float *ssrc, uint32_t bytes) {
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(ssrc);
@@ -68,89 +83,48 @@ __device__ __forceinline__ void sphere_span(float c, float rho, float inv_res, i
     hi = min(n - 1, (int)floorf(fminf(b, (float)n)));
 }
 
-// One item's contribution to a warp's region (plane i, rows [jg0, jg1]):
-// the voxels of its box cross-section that can lie inside its cutoff sphere.
-// Lane -> (row offset r, column kk), column fixed per item.
-template <bool BINARY, bool VECTOR>
-__device__ __forceinline__ void visit_item(const FwdItem &it, const BinItem &bi, int i, int jg0,
-                                           int jg1, float *accw, int D, double res, float resf,
-                                           float resl, float inv_res, double ox, double oy,
-                                           double oz, int lane) {
+// Phase A for one item: does it touch plane i, rows [jg0, jg1] inside its
+// cutoff sphere?  If so fill the slot.
+__device__ __forceinline__ bool plan_visit(const FwdItem &it, int i, int jg0, int jg1, int j0,
+                                           int D, float resf, float resl, float inv_res,
+                                           Slot &S) {
     const int4 bx = *reinterpret_cast<const int4 *>(&it.ibox);
     const int ilo = box_lo(bx.x);
-    if (i < ilo || i > box_hi(bx.x)) return;
+    if (i < ilo || i > box_hi(bx.x)) return false;
     const int jlo_b = box_lo(bx.y), klo_b = box_lo(bx.z);
     const int jlo = max(jlo_b, jg0), jhi = min(box_hi(bx.y), jg1);
-    if (jlo > jhi) return;
+    if (jlo > jhi) return false;
     const float4 P = *reinterpret_cast<const float4 *>(&it.cxh);
     const float4 Q = *reinterpret_cast<const float4 *>(&it.cxl);
     const float4 R = *reinterpret_cast<const float4 *>(&it.dzr);
     const float cut = R.x;
-    // plane offset dx (f32, ~1 ulp) and the sphere cross-section radius
     const float fi = (float)(i - ilo);
     const float dx = fmaf(fi, resf, P.x) + fmaf(fi, resl, Q.x);
     const float rho2 = fmaf(-dx, dx, cut * cut);
-    if (rho2 < -1e-5f * cut * cut) return;
+    if (rho2 < -1e-5f * cut * cut) return false;
     const float rho = fmaf(fast_sqrt(fmaxf(rho2, 0.0f)), 1.00002f, 1e-4f * cut);
     int jr0, jr1, kr0, kr1;
     sphere_span(P.y + Q.y, rho, inv_res, box_hi(bx.y) - jlo_b + 1, jr0, jr1);
     sphere_span(P.z + Q.z, rho, inv_res, box_hi(bx.z) - klo_b + 1, kr0, kr1);
     jr0 = max(jr0, jlo - jlo_b);
     jr1 = min(jr1, jhi - jlo_b);
-    if (jr0 > jr1 || kr0 > kr1) return;
-    const int nj = jr1 - jr0 + 1, nk = kr1 - kr0 + 1;
-    float *arow = accw + (size_t)(jlo_b + jr0) * D + klo_b;
-    if (BINARY) {
-        // _kernels.py:87-98 (index) / 180-192 (vector): exact f64, no contraction
-        const float w = R.z;
-        const double dxd = __dsub_rn(__dadd_rn(ox, __dmul_rn((double)i, res)), bi.x);
-        const double dx2 = __dmul_rn(dxd, dxd);
-        for (int kb = 0; kb < nk; kb += 32) {
-            const int nks = min(32, nk - kb);
-            const float inv = __frcp_rn((float)nks);
-            const int rpi = small_div(32, inv);
-            const int r = small_div(lane, inv), kk = kr0 + kb + lane - r * nks;
-            if (r >= rpi) continue;
-            const double dz = __dsub_rn(__dadd_rn(oz, __dmul_rn((double)(klo_b + kk), res)), bi.z);
-            const double dz2 = __dmul_rn(dz, dz);
-            float *ap = arow + kk + (size_t)r * D;
-            for (int jj = r; jj < nj; jj += rpi, ap += (size_t)rpi * D) {
-                const double dy = __dsub_rn(
-                    __dadd_rn(oy, __dmul_rn((double)(jlo_b + jr0 + jj), res)), bi.y);
-                const double d2 = __dadd_rn(__dadd_rn(dx2, __dmul_rn(dy, dy)), dz2);
-                if (d2 <= bi.r2) {
-                    if (VECTOR) *ap = fmaxf(*ap, w);
-                    else *ap = 1.0f;
-                }
-            }
-        }
-    } else {
-        // _kernels.py:99-106: Gaussian core to d0, quadratic tail to the cutoff
-        const float cexp = P.w, d02 = Q.w, qa = R.y, w = R.z;
-        const float dx2 = dx * dx;
-        for (int kb = 0; kb < nk; kb += 32) {
-            const int nks = min(32, nk - kb);
-            const float inv = __frcp_rn((float)nks);
-            const int rpi = small_div(32, inv);
-            const int r = small_div(lane, inv), kk = kr0 + kb + lane - r * nks;
-            if (r >= rpi) continue;
-            const float fk = (float)kk;
-            const float dz = fmaf(fk, resf, P.z) + fmaf(fk, resl, Q.z);
-            const float b2 = fmaf(dz, dz, dx2);
-            const float rpif = (float)rpi;
-            float *ap = arow + kk + (size_t)r * D;
-            float jf = (float)(jr0 + r);
-            for (int jj = r; jj < nj; jj += rpi, jf += rpif, ap += (size_t)rpi * D) {
-                const float dy = fmaf(jf, resf, P.y) + fmaf(jf, resl, Q.y);
-                const float d2 = fmaf(dy, dy, b2);
-                const float g = fast_ex2(d2 * cexp);
-                const float t = fmaxf(cut - fast_sqrt(d2), 0.0f);
-                const float v = d2 <= d02 ? g : qa * t * t;
-                *ap = fmaf(w, v, *ap);
-            }
-        }
-    }
-    __syncwarp();
+    if (jr0 > jr1 || kr0 > kr1) return false;
+    const int nk = kr1 - kr0 + 1;
+    S.yh = P.y;
+    S.yl = Q.y;
+    S.zh = P.z;
+    S.zl = Q.z;
+    S.dx2 = dx * dx;
+    S.cexp = P.w;
+    S.d02 = Q.w;
+    S.cut = cut;
+    S.qa = R.y;
+    S.w = R.z;
+    S.jspan = jr0 | ((jr1 - jr0 + 1) << 16);
+    S.kspan = kr0 | (nk << 16);
+    S.arow = (jlo_b + jr0 - j0) * D + klo_b;
+    S.rpi = 32 / min(32, nk);
+    return true;
 }
 
 template <bool BINARY, bool VECTOR>
@@ -167,9 +141,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const FwdArgs A) {
     const int32_t *co = A.chan_off + (size_t)e * (A.C + 1) + c;
     const int cs = co[0], ce = co[1];
 
-    if (cs == ce) {  // no item of this channel: zeros
-        if (A.bulk) {
-            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (cs == ce) {  // no item of this channel: stream zeros
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (A.bulk && TJv == D) {
+            // the tile's planes are one contiguous run
+            float4 *o = reinterpret_cast<float4 *>(obase);
+            const int n4 = (TIv * chunk) >> 2;
+            for (int q = tid; q < n4; q += kThreads) __stcs(o + q, z);
+        } else if (A.bulk) {
             for (int p = 0; p < TIv; p++) {
                 float4 *o = reinterpret_cast<float4 *>(obase + p * plane);
                 for (int q = tid; q < (chunk >> 2); q += kThreads) __stcs(o + q, z);
@@ -182,63 +161,134 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const FwdArgs A) {
     }
 
     float *acc = reinterpret_cast<float *>(smem);
-    FwdItem *list = reinterpret_cast<FwdItem *>(smem + A.acc_floats * 4);
-    BinItem *blist = reinterpret_cast<BinItem *>(list + kCap);
-    int *wcount = reinterpret_cast<int *>(BINARY ? (unsigned char *)(blist + kCap)
-                                                 : (unsigned char *)blist);
-    {
-        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 *a4 = reinterpret_cast<float4 *>(acc);
-        for (int q = tid; q < (int)(A.acc_floats >> 2); q += kThreads) a4[q] = z;
-    }
-
-    // this warp's region: plane p, global rows [jg0, jg1]
-    const int p = warp / A.wpp, part = warp - (warp / A.wpp) * A.wpp;
+    Slot *slots = reinterpret_cast<Slot *>(smem + A.acc_floats * 4) + warp * 32;
+    // this warp's region: plane p, global rows [jg0, jg1]; warps are
+    // independent until the final store
+    const int p = warp / A.wpp, part = warp - p * A.wpp;
     const int i = i0 + p;
     const int jg0 = j0 + part * A.rpw, jg1 = j0 + min((part + 1) * A.rpw, TJv) - 1;
     const bool region_ok = p < TIv && jg0 <= jg1;
-    float *accw = acc + (size_t)p * TJ * D - (size_t)j0 * D;  // accw[j * D + k]
-    const double res = A.res;
-    const float resf = A.resf, resl = A.resl, inv_res = A.inv_res;
-    const double ox = A.origins[3 * e + 0], oy = A.origins[3 * e + 1], oz = A.origins[3 * e + 2];
-    const int ti_hi = i0 + TIv - 1, tj_hi = j0 + TJv - 1;
-    const unsigned lt = (1u << lane) - 1u;
-
-    int count = 0;
-    __syncthreads();
-    for (int base = cs; base < ce; base += kThreads) {
-        const int it = base + tid;
-        bool keep = false;
-        if (it < ce) {
-            const int2 bx = *reinterpret_cast<const int2 *>(&A.sorted[it].ibox);
-            keep = box_lo(bx.x) <= ti_hi && box_hi(bx.x) >= i0 && box_lo(bx.y) <= tj_hi &&
-                   box_hi(bx.y) >= j0;
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) wcount[warp] = __popc(m);
-        __syncthreads();
-        int before = 0, total = 0;
-#pragma unroll
-        for (int w = 0; w < kWarps; w++) {
-            const int n = wcount[w];
-            before += (w < warp) ? n : 0;
-            total += n;
-        }
-        if (keep) {
-            const int pos = count + before + __popc(m & lt);
-            list[pos] = A.sorted[it];
-            if (BINARY) blist[pos] = A.bsorted[it];
-        }
-        count += total;
-        __syncthreads();
-        if (count > kCap - kThreads || base + kThreads >= ce) {
-            if (region_ok) {
-                for (int idx = 0; idx < count; idx++)
-                    visit_item<BINARY, VECTOR>(list[idx], blist[idx], i, jg0, jg1, accw, D, res,
-                                               resf, resl, inv_res, ox, oy, oz, lane);
+    float *accp = acc + (size_t)p * TJ * D;  // plane p of the tile, row j at (j - j0) * D
+    if (region_ok) {
+        {
+            const int nf = (jg1 - jg0 + 1) * D;
+            if ((D & 3) == 0) {
+                float4 *r0 = reinterpret_cast<float4 *>(accp + (size_t)(jg0 - j0) * D);
+                const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int q = lane; q < (nf >> 2); q += 32) r0[q] = z;
+            } else {
+                float *rs = accp + (size_t)(jg0 - j0) * D;
+                for (int q = lane; q < nf; q += 32) rs[q] = 0.0f;
             }
-            __syncthreads();
-            count = 0;
+        }
+        const double res = A.res;
+        const float resf = A.resf, resl = A.resl, inv_res = A.inv_res;
+        const double ox = A.origins[3 * e + 0], oy = A.origins[3 * e + 1],
+                     oz = A.origins[3 * e + 2];
+        for (int base = cs; base < ce; base += 32) {
+            // ---- phase A: lane t plans item base + t ----
+            const int it = base + lane;
+            bool hit = false;
+            if (it < ce) {
+                const int2 bx = A.sbox[it];
+                if (box_lo(bx.x) <= i && box_hi(bx.x) >= i && box_lo(bx.y) <= jg1 &&
+                    box_hi(bx.y) >= jg0) {
+                    Slot S;
+                    hit = plan_visit(A.sorted[it], i, jg0, jg1, j0, D, resf, resl, inv_res, S);
+                    if (hit) {
+                        S.src = it;
+                        slots[lane] = S;
+                    }
+                }
+            }
+            unsigned m = __ballot_sync(0xffffffffu, hit);
+            __syncwarp();
+            // ---- phase B: items in order, all lanes scatter ----
+            while (m) {
+                const int t = __ffs(m) - 1;
+                m &= m - 1;
+                const float4 S0 = *reinterpret_cast<const float4 *>(&slots[t].yh);
+                const float4 S1 = *reinterpret_cast<const float4 *>(&slots[t].dx2);
+                const float4 S2 = *reinterpret_cast<const float4 *>(&slots[t].qa);
+                const int4 S3 = *reinterpret_cast<const int4 *>(&slots[t].arow);
+                const int jr0 = box_lo(__float_as_int(S2.z)), nj = box_hi(__float_as_int(S2.z));
+                const int kr0 = box_lo(__float_as_int(S2.w)), nk = box_hi(__float_as_int(S2.w));
+                const int rpi = S3.y;
+                const int nks = min(32, nk);
+                const float inv = __frcp_rn((float)nks);
+                const int r = small_div(lane, inv);
+                if (BINARY) {
+                    // _kernels.py:87-98 (index) / 180-192 (vector): exact f64, no contraction
+                    const BinItem bi = A.bsorted[S3.z];
+                    const int4 bx = *reinterpret_cast<const int4 *>(&A.sorted[S3.z].ibox);
+                    const int jb = box_lo(bx.y) + jr0, kb0 = box_lo(bx.z) + kr0;
+                    const double dxd =
+                        __dsub_rn(__dadd_rn(ox, __dmul_rn((double)i, res)), bi.x);
+                    const double dx2 = __dmul_rn(dxd, dxd);
+                    const float w = S2.y;
+                    for (int kb = 0; kb < nk; kb += 32) {
+                        const int nkb = min(32, nk - kb);
+                        const float invb = __frcp_rn((float)nkb);
+                        const int rpb = small_div(32, invb);
+                        const int rr = small_div(lane, invb), kk = kb + lane - rr * nkb;
+                        if (rr >= rpb) continue;
+                        const double dz =
+                            __dsub_rn(__dadd_rn(oz, __dmul_rn((double)(kb0 + kk), res)), bi.z);
+                        const double dz2 = __dmul_rn(dz, dz);
+                        float *ap = accp + S3.x + kr0 + kk + (size_t)rr * D;
+                        for (int jj = rr; jj < nj; jj += rpb, ap += (size_t)rpb * D) {
+                            const double dy = __dsub_rn(
+                                __dadd_rn(oy, __dmul_rn((double)(jb + jj), res)), bi.y);
+                            const double d2 = __dadd_rn(__dadd_rn(dx2, __dmul_rn(dy, dy)), dz2);
+                            if (d2 <= bi.r2) {
+                                if (VECTOR) *ap = fmaxf(*ap, w);
+                                else *ap = 1.0f;
+                            }
+                        }
+                    }
+                } else if (nk <= 32) {
+                    // _kernels.py:99-106: Gaussian core to d0, quadratic tail to the cutoff
+                    if (r < rpi) {
+                        const int kk = kr0 + lane - r * nks;
+                        const float fk = (float)kk;
+                        const float dz = fmaf(fk, resf, S0.z) + fmaf(fk, resl, S0.w);
+                        const float b2 = fmaf(dz, dz, S1.x);
+                        const float cexp = S1.y, d02 = S1.z, cut = S1.w, qa = S2.x, w = S2.y;
+                        const float rpif = (float)rpi;
+                        float *ap = accp + S3.x + kk + r * D;
+                        const int step = rpi * D;
+                        float jf = (float)(jr0 + r);
+                        for (int jj = r; jj < nj; jj += rpi, jf += rpif, ap += step) {
+                            const float dy = fmaf(jf, resf, S0.x) + fmaf(jf, resl, S0.y);
+                            const float d2 = fmaf(dy, dy, b2);
+                            const float g = fast_ex2(d2 * cexp);
+                            const float t2 = fmaxf(cut - fast_sqrt(d2), 0.0f);
+                            const float v = d2 <= d02 ? g : qa * t2 * t2;
+                            *ap = fmaf(w, v, *ap);
+                        }
+                    }
+                } else {
+                    // > 32 columns (very fine grids): one row pass per 32 columns
+                    const float cexp = S1.y, d02 = S1.z, cut = S1.w, qa = S2.x, w = S2.y;
+                    for (int kb = lane; kb < nk; kb += 32) {
+                        const int kk = kr0 + kb;
+                        const float fk = (float)kk;
+                        const float dz = fmaf(fk, resf, S0.z) + fmaf(fk, resl, S0.w);
+                        const float b2 = fmaf(dz, dz, S1.x);
+                        float *ap = accp + S3.x + kk;
+                        for (int jj = 0; jj < nj; jj++, ap += D) {
+                            const float jf = (float)(jr0 + jj);
+                            const float dy = fmaf(jf, resf, S0.x) + fmaf(jf, resl, S0.y);
+                            const float d2 = fmaf(dy, dy, b2);
+                            const float g = fast_ex2(d2 * cexp);
+                            const float t2 = fmaxf(cut - fast_sqrt(d2), 0.0f);
+                            const float v = d2 <= d02 ? g : qa * t2 * t2;
+                            *ap = fmaf(w, v, *ap);
+                        }
+                    }
+                }
+                __syncwarp();
+            }
         }
     }
 
@@ -247,8 +297,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const FwdArgs A) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
         if (tid == 0) {
-            for (int pp = 0; pp < TIv; pp++)
-                bulk_store(obase + pp * plane, acc + (size_t)pp * TJ * D, (uint32_t)chunk * 4u);
+            if (TJv == D) {
+                bulk_store(obase, acc, (uint32_t)(TIv * chunk) * 4u);
+            } else {
+                for (int pp = 0; pp < TIv; pp++)
+                    bulk_store(obase + pp * plane, acc + (size_t)pp * TJ * D, (uint32_t)chunk * 4u);
+            }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
@@ -265,8 +319,8 @@ struct FwdConfig {
     size_t acc_floats, smem;
 };
 
-FwdConfig choose_config(int D, bool binary) {
-    const size_t budget = 80 * 1024;
+FwdConfig choose_config(int D) {
+    const size_t budget = 80 * 1024;  // acc; + 16 KB of slots -> 2 CTAs per SM
     const size_t plane = (size_t)D * D * 4;
     FwdConfig cfg{};
     int TI = 8;
@@ -278,8 +332,7 @@ FwdConfig choose_config(int D, bool binary) {
     cfg.TJ = std::min(TJ, D);
     cfg.rpw = (cfg.TJ + cfg.wpp - 1) / cfg.wpp;
     cfg.acc_floats = align_up((size_t)cfg.TI * cfg.TJ * D, 32);
-    cfg.smem = cfg.acc_floats * 4 + (size_t)kCap * (sizeof(FwdItem) + (binary ? sizeof(BinItem) : 0)) +
-               64;
+    cfg.smem = cfg.acc_floats * 4 + (size_t)kWarps * 32 * sizeof(Slot);
     return cfg;
 }
 
@@ -299,11 +352,12 @@ gm_status launch(const FwdArgs &A, const FwdConfig &cfg, int nex, cudaStream_t s
 gm_status forward_impl(const gm_params *p, const gm_batch *b, const Workspace &ws, float *out,
                        cudaStream_t s) {
     const int D = p->npts;
-    const FwdConfig cfg = choose_config(D, p->binary != 0);
+    const FwdConfig cfg = choose_config(D);
     if (cfg.smem > 227 * 1024) return gm_fail(GM_ERR_INVALID, "grid too large for one tile row");
     FwdArgs A;
     A.sorted = ws.sorted;
     A.bsorted = ws.bsorted;
+    A.sbox = ws.sbox;
     A.chan_off = ws.chan_off;
     A.origins = b->origins;
     A.out = out;

@@ -129,6 +129,7 @@ struct BinArgs {
     const int32_t *ex_item_start, *ex_item_end;
     FwdItem *sorted;
     BinItem *bsorted;
+    int2 *sbox;
     int32_t *chan_off;
     int C;
     int binary;
@@ -179,8 +180,9 @@ __global__ void __launch_bounds__(1024) k_bin(const BinArgs A) {
         const int c = chs[q];
         if (c < 0) continue;
         const int dst = cnt[c] + rank[q];
-        reinterpret_cast<int4 *>(A.sorted + dst)[part] =
-            reinterpret_cast<const int4 *>(A.items + is + q)[part];
+        const int4 v = reinterpret_cast<const int4 *>(A.items + is + q)[part];
+        reinterpret_cast<int4 *>(A.sorted + dst)[part] = v;
+        if (part == 3) A.sbox[dst] = make_int2(v.x, v.y);  // ibox, jbox
         if (A.binary && part < 2)
             reinterpret_cast<int4 *>(A.bsorted + dst)[part] =
                 reinterpret_cast<const int4 *>(A.bitems + is + q)[part];
@@ -213,6 +215,7 @@ gm_status prepare_impl(const gm_params *p, const gm_batch *b, const Workspace &w
         B.ex_item_end = b->ex_item_end;
         B.sorted = ws.sorted;
         B.bsorted = ws.bsorted;
+        B.sbox = ws.sbox;
         B.chan_off = ws.chan_off;
         B.C = b->nchannels;
         B.binary = p->binary;
