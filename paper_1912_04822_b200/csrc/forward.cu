@@ -48,9 +48,9 @@ struct __align__(16) Slot {
     float qa, w;               // quadratic coefficient, weight
     int jspan, kspan;          // first row / column relative to the box corner | count << 16
     int arow;                  // accumulator offset of (first row, box column 0)
-    int rpi;                   // rows per pass = 32 / min(32, columns)
+    int rpi;                   // columns per pass = min(32, columns)
     int src;                   // item index (binary mode re-reads the f64 record)
-    int pad;
+    int pad;                   // bits of 1 / (columns per pass)
 };
 static_assert(sizeof(Slot) == 64, "Slot must be 64 bytes");
 
@@ -123,11 +123,12 @@ __device__ __forceinline__ bool plan_visit(const FwdItem &it, int i, int jg0, in
     S.jspan = jr0 | ((jr1 - jr0 + 1) << 16);
     S.kspan = kr0 | (nk << 16);
     S.arow = (jlo_b + jr0 - j0) * D + klo_b;
-    S.rpi = 32 / min(32, nk);
+    S.rpi = min(32, nk);  // columns per pass
+    S.pad = __float_as_int(__frcp_rn((float)S.rpi));
     return true;
 }
 
-template <bool BINARY, bool VECTOR>
+template <bool BINARY, bool VECTOR, bool RESL>
 __global__ void __launch_bounds__(kThreads, 2) k_forward(const FwdArgs A) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -213,10 +214,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const FwdArgs A) {
                 const int4 S3 = *reinterpret_cast<const int4 *>(&slots[t].arow);
                 const int jr0 = box_lo(__float_as_int(S2.z)), nj = box_hi(__float_as_int(S2.z));
                 const int kr0 = box_lo(__float_as_int(S2.w)), nk = box_hi(__float_as_int(S2.w));
-                const int rpi = S3.y;
-                const int nks = min(32, nk);
-                const float inv = __frcp_rn((float)nks);
-                const int r = small_div(lane, inv);
+                const int nks = S3.y;
+                const float inv = __int_as_float(S3.w);  // 1/nks (approximate, exact enough)
+                const int r = small_div(lane, inv), rpi = small_div(32, inv);
                 if (BINARY) {
                     // _kernels.py:87-98 (index) / 180-192 (vector): exact f64, no contraction
                     const BinItem bi = A.bsorted[S3.z];
@@ -259,7 +259,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_forward(const FwdArgs A) {
                         const int step = rpi * D;
                         float jf = (float)(jr0 + r);
                         for (int jj = r; jj < nj; jj += rpi, jf += rpif, ap += step) {
-                            const float dy = fmaf(jf, resf, S0.x) + fmaf(jf, resl, S0.y);
+                            const float dy = RESL ? fmaf(jf, resf, S0.x) + fmaf(jf, resl, S0.y)
+                                                  : fmaf(jf, resf, S0.x) + S0.y;
                             const float d2 = fmaf(dy, dy, b2);
                             const float g = fast_ex2(d2 * cexp);
                             const float t2 = fmaxf(cut - fast_sqrt(d2), 0.0f);
@@ -336,9 +337,9 @@ FwdConfig choose_config(int D) {
     return cfg;
 }
 
-template <bool BIN, bool VEC>
+template <bool BIN, bool VEC, bool RESL>
 gm_status launch(const FwdArgs &A, const FwdConfig &cfg, int nex, cudaStream_t s) {
-    auto kern = k_forward<BIN, VEC>;
+    auto kern = k_forward<BIN, VEC, RESL>;
     CUDA_TRY(gm_ensure_smem((const void *)kern, (int)cfg.smem));
     const int ntiles = ((A.D + cfg.TI - 1) / cfg.TI) * A.ntj;
     dim3 grid(ntiles * A.C, nex);
@@ -375,7 +376,9 @@ gm_status forward_impl(const gm_params *p, const gm_batch *b, const Workspace &w
     A.bulk = (D % 4) == 0 && ((uintptr_t)out % 16) == 0;
     A.acc_floats = cfg.acc_floats;
     if (p->binary)
-        return b->vector_mode ? launch<true, true>(A, cfg, b->nexamples, s)
-                              : launch<true, false>(A, cfg, b->nexamples, s);
-    return launch<false, false>(A, cfg, b->nexamples, s);
+        return b->vector_mode ? launch<true, true, false>(A, cfg, b->nexamples, s)
+                              : launch<true, false, false>(A, cfg, b->nexamples, s);
+    // resolutions exactly representable in f32 (0.5, 0.25, 0.375 ...) drop the lo term
+    return A.resl != 0.0f ? launch<false, false, true>(A, cfg, b->nexamples, s)
+                          : launch<false, false, false>(A, cfg, b->nexamples, s);
 }
