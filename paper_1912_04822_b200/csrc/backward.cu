@@ -189,7 +189,7 @@ constexpr int kSub = 16;                // table entries per axis
 constexpr int kAtomsPerBlock = 256 / kLPA;
 
 struct SmallTables {
-    double dx[kSub], ex[kSub], dy[kSub], ey[kSub], dz[kSub], ez[kSub];
+    double dx[kSub], ex[kSub], dy[kSub], ey[kSub], dz[kSub], ez[kSub], ezdz[kSub];
 };
 
 __global__ void __launch_bounds__(256, 2) k_backward_index(const BwdArgs P) {
@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(256, 2) k_backward_index(const BwdArgs P) {
                         double *et = ax == 0 ? T.ex : (ax == 1 ? T.ey : T.ez);
                         dt[q] = d;
                         et[q] = E;
+                        if (ax == 2) T.ezdz[q] = E * d;
                     }
                 }
                 __syncwarp(gmask);
@@ -264,33 +265,54 @@ __global__ void __launch_bounds__(256, 2) k_backward_index(const BwdArgs P) {
                         min(nk - 1, (int)floorf(fminf((dz0 + rho) * inv_res, (float)nk)));
                     const double exy = T.ex[ii] * T.ey[jj] * m4inv_r2;
                     const float *gr = gsub + ((size_t)ii * D + jj) * D;
+                    // Gaussian core of the row: voxels certainly within d0 (shrunk
+                    // span; the separable factors reduce them to two FMAs each)
+                    int kc0 = khi + 1, kc1 = khi;
+                    const double remc = d02 - b2;
+                    if (remc > 0.0) {
+                        const float rc = fmaf(sqrtf((float)remc), 0.99999f, -1e-4f * (float)res);
+                        if (rc > 0.0f) {
+                            kc0 = max(klo, (int)ceilf((dz0 - rc) * inv_res));
+                            kc1 = min(khi, (int)floorf((dz0 + rc) * inv_res));
+                            if (kc0 > kc1) {
+                                kc0 = khi + 1;
+                                kc1 = khi;
+                            }
+                        }
+                    }
                     // the whole row span first (<= kSub loads in flight), then the math
                     float g[kSub];
 #pragma unroll
                     for (int q = 0; q < kSub; q++)
                         g[q] = (klo + q <= khi) ? __ldg(gr + klo + q) : 0.0f;
+                    double cs = 0.0, csz = 0.0, ts = 0.0, tsz = 0.0;
 #pragma unroll
                     for (int q = 0; q < kSub; q++) {
-                        if (klo + q > khi) break;
                         const int kk = klo + q;
-                        const double dz = T.dz[kk];
-                        const double d2 = fma(dz, dz, b2);
-                        const bool in = d2 > 0.0 && d2 < A.dzr2;
-                        const double gv = in ? (double)g[q] : 0.0;
-                        const double rd = rsqrt_d(d2);
-                        const double sq = gv * (qa2 * fma(d2, rd, -A.dzr)) * rd;
-                        const double sg = gv * (exy * T.ez[kk]);
-                        const double sc = d2 <= d02 ? sg : sq;
-                        if (q & 1) {
-                            ax1 = fma(sc, dx, ax1);
-                            ay1 = fma(sc, dy, ay1);
-                            az1 = fma(sc, dz, az1);
+                        if (kk > khi) break;
+                        const double gq = (double)g[q];
+                        if (kk >= kc0 && kk <= kc1) {
+                            cs = fma(gq, T.ez[kk], cs);
+                            csz = fma(gq, T.ezdz[kk], csz);
                         } else {
-                            ax0 = fma(sc, dx, ax0);
-                            ay0 = fma(sc, dy, ay0);
-                            az0 = fma(sc, dz, az0);
+                            // shell and boundary voxels: exact f64 classification
+                            const double dz = T.dz[kk];
+                            const double d2 = fma(dz, dz, b2);
+                            const bool in = d2 > 0.0 && d2 < A.dzr2;
+                            const double gv = in ? gq : 0.0;
+                            const double rd = rsqrt_d(d2);
+                            const double sq = gv * qa2 * fma(-A.dzr, rd, 1.0);
+                            const double sg = gv * (exy * T.ez[kk]);
+                            const double sc = d2 <= d02 ? sg : sq;
+                            ts += sc;
+                            tsz = fma(sc, dz, tsz);
                         }
                     }
+                    // slope/d * offset summed over the row: core terms share exy
+                    const double srow = fma(exy, cs, ts);
+                    ax0 = fma(srow, dx, ax0);
+                    ay0 = fma(srow, dy, ay0);
+                    az0 = fma(exy, csz, az0 + tsz);
                 }
             }
     double gx = ax0 + ax1, gy = ay0 + ay1, gz = az0 + az1;
