@@ -447,7 +447,8 @@ static gm_status run_host_backward(double *coord_grad, double *type_grad, const 
     b.origins = (const double *)(d + o_orig);
     gm_params p = host_params(npts, res, grm, rmult, 0, rti);
     // positions only (no transform); items are not needed by the backward
-    gm_status st = prepare_impl(&p, &b, ws_of(d + o_ws, &b), nullptr, false);
+    // index mode: the backward reuses the forward items' boxes
+    gm_status st = prepare_impl(&p, &b, ws_of(d + o_ws, &b), nullptr, !vector_mode);
     if (st) return st;
     st = gm_backward(&p, &b, d + o_ws, (const float *)(d + o_gg), (float *)(d + o_cg),
                                vector_mode ? (float *)(d + o_tg) : nullptr, nullptr);

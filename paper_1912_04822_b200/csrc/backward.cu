@@ -16,6 +16,8 @@
 //    1e-6 gate on near-cancelling components).  The quadratic tail needs 1/d:
 //    an f32 MUFU estimate refined by one f64 Newton step.  Two accumulator
 //    chains per lane, then a warp-shuffle reduction: no atomics, deterministic.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace {
@@ -31,6 +33,9 @@ struct BwdArgs {
     const float *grid_grad;
     float *coord_grad;
     float *type_grad;
+    const FwdItem *items;  // index mode: item a == atom a; its box (cut rmult*r) is reused
+    double eg;             // exp(-2 grm^2), a batch constant (_kernels.py:224)
+    int dbg;
 };
 
 struct Tables {
@@ -49,17 +54,37 @@ __device__ __forceinline__ double offs(double x, double o, int i, double res) {
     return __dsub_rn(x, __dadd_rn(o, __dmul_rn((double)i, res)));
 }
 
+__device__ __forceinline__ float approx_sqrt(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ float approx_rsqrt(float x) {
     float y;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
 
-// 1/sqrt(d2) to ~1e-13 relative: f32 MUFU estimate + one f64 Newton step.
+// 1/sqrt(d2) to ~1e-13 relative: the f64 MUFU estimate (MUFU.RSQ64H, ~2^-22)
+// + one f64 Newton step -- one XU op, no f32 <-> f64 conversions.
 __device__ __forceinline__ double rsqrt_d(double d2) {
-    const double y0 = (double)approx_rsqrt((float)d2);
+    double y0;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(d2));
     const double e = fma(-d2 * y0, y0, 1.0);
     return fma(0.5 * y0, e, y0);
+}
+
+// Exact float -> double widening on the integer pipe (F2F.F64.F32 runs on the
+// XU, the backward's bottleneck).  Zeros and denormals map to signed zero
+// (grid gradients below 1e-38 contribute nothing at f32 output precision);
+// inf / NaN are not expected in gradients.
+__device__ __forceinline__ double widen(float f) {
+    const unsigned u = __float_as_uint(f);
+    const bool nz = (u & 0x7f800000u) != 0u;
+    const unsigned hi = (u & 0x80000000u) | (nz ? ((u >> 3) & 0x0fffffffu) + (896u << 20) : 0u);
+    const unsigned lo = nz ? (u << 29) : 0u;
+    return __hiloint2double((int)hi, (int)lo);
 }
 
 // floor(a / b) for 0 <= a < 2^16, 1 <= b <= 64 (float reciprocal, exact here).
@@ -178,155 +203,204 @@ __device__ __forceinline__ void store_coord(const BwdArgs &P, int a, int lane, d
 }
 
 // ---------------------------------------------------------------------------
-// Index types: kLPA lanes per atom.  The lanes of an atom share per-axis
-// tables (offset, f64 Gaussian factor; kSub entries per axis, sub-boxes for
-// larger boxes) and split its (i, j) rows round-robin; each row walks only
-// its k span inside the cutoff sphere, two voxels at a time, branch-free
-// (voxels outside the sphere load nothing and add an exact 0).
+// Index types: one warp per atom, flattened walk.
+//
+// The atom's box is cut into chunks of <= kRows (i, j) rows.  Phase 1: lanes
+// compute each row's k span inside the cutoff sphere and a warp scan lays the
+// non-empty rows out back to back (row table in shared memory: start offset,
+// k origin, b2 = dx^2 + dy^2, dx, dy, Gaussian factor).  Phase 2: the warp
+// walks the flattened list 32 voxels at a time -- every lane has a voxel, so
+// no lane idles on short rows; a lane finds its row from a bit mask of the
+// row starts inside the window (REDUX + popc).  Geometry and accumulation in
+// f64; the tail's 1/d from MUFU.RSQ64H + one Newton step.
 // ---------------------------------------------------------------------------
-constexpr int kLPA = 4;                 // lanes per atom
-constexpr int kSub = 16;                // table entries per axis
-constexpr int kAtomsPerBlock = 256 / kLPA;
+constexpr int kBwdWarps = 4;
+constexpr int kRows = 96;     // rows per chunk
+constexpr int kTab = 32;      // table entries per axis (sub-box edge)
 
-struct SmallTables {
-    double dx[kSub], ex[kSub], dy[kSub], ey[kSub], dz[kSub], ez[kSub], ezdz[kSub];
+struct __align__(16) RowEntry {
+    int start;   // offset of the row's first voxel in the flattened list
+    int kpack;   // k0 (relative to the sub-box) | (i_rel << 8) | (j_rel << 16)
+    double b2;   // dx^2 + dy^2
+    double exy;  // Ex * Ey * (-4 / r^2)
+    double dx, dy;
 };
 
-__global__ void __launch_bounds__(256, 2) k_backward_index(const BwdArgs P) {
-    __shared__ SmallTables tabs[kAtomsPerBlock];
-    const int sub = threadIdx.x & (kLPA - 1);
-    const int slot = threadIdx.x / kLPA;
-    const int a = blockIdx.x * kAtomsPerBlock + slot;
+struct WarpBwd {
+    double dz[kTab], ez[kTab], dx[kTab], ex[kTab], dy[kTab], ey[kTab];
+    RowEntry rows[kRows];
+};
+
+__global__ void __launch_bounds__(kBwdWarps * 32) k_backward_index(const BwdArgs P) {
+    __shared__ WarpBwd wsm[kBwdWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int a = blockIdx.x * kBwdWarps + warp;
     const gm_batch &b = P.b;
-    const bool live = a < b.natoms;
+    if (a >= b.natoms) return;
+    WarpBwd &W = wsm[warp];
     const int D = P.p.npts;
     const double res = P.p.resolution, grm = P.p.gaussian_radius_multiple;
     const float inv_res = (float)(1.0 / res);
-    SmallTables &T = tabs[slot];
-    // the lanes of one atom (they share T); atoms of a warp may run different
-    // sub-box loops, so synchronise only the group
-    const unsigned gmask = ((1u << kLPA) - 1u) << ((threadIdx.x & 31) & ~(kLPA - 1));
-    double ax0 = 0.0, ay0 = 0.0, az0 = 0.0, ax1 = 0.0, ay1 = 0.0, az1 = 0.0;
     Atom A;
-    bool any = false;
-    int e = 0, c = 0;
-    double d02 = 0.0, qa2 = 0.0, m4inv_r2 = 0.0;
-    if (live) {
-        int s;
-        load_atom(P, a, A, s, e);
-        c = b.set_choff[s] + b.atom_type[a];
-        const double r = b.atom_radius[a];
-        const double d0 = grm * r;
-        d02 = d0 * d0;
-        const double q0 = (2.0 * grm) / r;
-        qa2 = 2.0 * (exp((-2.0 * grm) * grm) * (q0 * q0));
-        m4inv_r2 = -4.0 / (r * r);
-        any = set_radius(A, r, P.p.radius_multiple, res, D);
-    }
-    const size_t D3 = (size_t)D * D * D;
-    const float *gbase = P.grid_grad + ((size_t)e * b.nchannels + c) * D3;
-    // sub-box loop bounds are uniform across the atom's lanes
-    const int si_end = any ? A.i1 : -1;
-    for (int si = any ? A.i0 : 0; si <= si_end; si += kSub)
-        for (int sj = A.j0; sj <= A.j1; sj += kSub)
-            for (int sk = A.k0; sk <= A.k1; sk += kSub) {
-                const int ni = min(kSub, A.i1 - si + 1), nj = min(kSub, A.j1 - sj + 1),
-                          nk = min(kSub, A.k1 - sk + 1);
-                __syncwarp(gmask);
-                for (int l = sub; l < 3 * kSub; l += kLPA) {
-                    const int ax = l / kSub, q = l - ax * kSub;
-                    const int n = ax == 0 ? ni : (ax == 1 ? nj : nk);
-                    if (q < n) {
-                        const double x = ax == 0 ? A.x : (ax == 1 ? A.y : A.z);
-                        const double o = ax == 0 ? A.ox : (ax == 1 ? A.oy : A.oz);
-                        const int i0 = ax == 0 ? si : (ax == 1 ? sj : sk);
-                        const double d = offs(x, o, i0 + q, res);
+    int s, e;
+    load_atom(P, a, A, s, e);
+    const int c = b.set_choff[s] + b.atom_type[a];
+    const double r = b.atom_radius[a];
+    const double d0 = grm * r, d02 = d0 * d0;
+    const double q0 = (2.0 * grm) / r;
+    const double qa2 = 2.0 * (P.eg * (q0 * q0));
+    const double m4inv_r2 = -4.0 / (r * r);
+    double gx0 = 0.0, gy0 = 0.0, gz0 = 0.0, gx1 = 0.0, gy1 = 0.0, gz1 = 0.0;
+    const unsigned lt = (1u << lane) - 1u;
+    // the forward item of this atom carries the same box (_kernels.py:225-227)
+    const int4 bx = *reinterpret_cast<const int4 *>(&P.items[a].ibox);
+    A.dzr = P.p.radius_multiple * r;
+    A.dzr2 = A.dzr * A.dzr;
+    A.m2inv_r2 = 0.5 * m4inv_r2;
+    A.i0 = box_lo(bx.x);
+    A.i1 = box_hi(bx.x);
+    A.j0 = box_lo(bx.y);
+    A.j1 = box_hi(bx.y);
+    A.k0 = box_lo(bx.z);
+    A.k1 = box_hi(bx.z);
+    (void)D;
+    if (A.i0 <= A.i1 && A.j0 <= A.j1 && A.k0 <= A.k1) {
+        const size_t D3 = (size_t)D * D * D;
+        const float *gbase = P.grid_grad + ((size_t)e * b.nchannels + c) * D3;
+        const double dzr = A.dzr, dzr2 = A.dzr2;
+        for (int si = A.i0; si <= A.i1; si += kTab)
+            for (int sj = A.j0; sj <= A.j1; sj += kTab)
+                for (int sk = A.k0; sk <= A.k1; sk += kTab) {
+                    const int ni = min(kTab, A.i1 - si + 1), nj = min(kTab, A.j1 - sj + 1),
+                              nk = min(kTab, A.k1 - sk + 1);
+                    __syncwarp();
+                    for (int l = lane; l < ni + nj + nk; l += 32) {
+                        const int ax = l < ni ? 0 : (l < ni + nj ? 1 : 2);
+                        const int q = l - (ax == 0 ? 0 : (ax == 1 ? ni : ni + nj));
+                        const double d = ax == 0 ? offs(A.x, A.ox, si + q, res)
+                                                 : (ax == 1 ? offs(A.y, A.oy, sj + q, res)
+                                                            : offs(A.z, A.oz, sk + q, res));
                         const double E = exp(A.m2inv_r2 * (d * d));
-                        double *dt = ax == 0 ? T.dx : (ax == 1 ? T.dy : T.dz);
-                        double *et = ax == 0 ? T.ex : (ax == 1 ? T.ey : T.ez);
+                        double *dt = ax == 0 ? W.dx : (ax == 1 ? W.dy : W.dz);
+                        double *et = ax == 0 ? W.ex : (ax == 1 ? W.ey : W.ez);
                         dt[q] = d;
                         et[q] = E;
-                        if (ax == 2) T.ezdz[q] = E * d;
                     }
-                }
-                __syncwarp(gmask);
-                const float inv_nj = __frcp_rn((float)nj);
-                const float dz0 = (float)T.dz[0];
-                const float *gsub = gbase + ((size_t)si * D + sj) * D + sk;
-                for (int row = sub; row < ni * nj; row += kLPA) {
-                    const int ii = idiv(row, inv_nj), jj = row - ii * nj;
-                    const double dx = T.dx[ii], dy = T.dy[jj];
-                    const double b2 = fma(dy, dy, dx * dx);
-                    const double rem = A.dzr2 - b2;
-                    if (rem <= 0.0) continue;
-                    const float rho = fmaf(sqrtf((float)rem), 1.0001f, 1e-5f * (float)A.dzr);
-                    const int klo = max(0, (int)ceilf(fmaxf((dz0 - rho) * inv_res, -1.0f)));
-                    const int khi =
-                        min(nk - 1, (int)floorf(fminf((dz0 + rho) * inv_res, (float)nk)));
-                    const double exy = T.ex[ii] * T.ey[jj] * m4inv_r2;
-                    const float *gr = gsub + ((size_t)ii * D + jj) * D;
-                    // Gaussian core of the row: voxels certainly within d0 (shrunk
-                    // span; the separable factors reduce them to two FMAs each)
-                    int kc0 = khi + 1, kc1 = khi;
-                    const double remc = d02 - b2;
-                    if (remc > 0.0) {
-                        const float rc = fmaf(sqrtf((float)remc), 0.99999f, -1e-4f * (float)res);
-                        if (rc > 0.0f) {
-                            kc0 = max(klo, (int)ceilf((dz0 - rc) * inv_res));
-                            kc1 = min(khi, (int)floorf((dz0 + rc) * inv_res));
-                            if (kc0 > kc1) {
-                                kc0 = khi + 1;
-                                kc1 = khi;
+                    __syncwarp();
+                    const float dz0 = (float)W.dz[0];
+                    const float inv_nj = __frcp_rn((float)nj);
+                    const float *gsub = gbase + ((size_t)si * D + sj) * D + sk;
+                    const int nrows_all = ni * nj;
+                    for (int rb = 0; rb < nrows_all; rb += kRows) {
+                        // ---- phase 1: row spans, compacted with a warp scan ----
+                        int nrow = 0, total = 0;
+                        const int rend = min(nrows_all, rb + kRows);
+                        for (int r0 = rb; r0 < rend; r0 += 32) {
+                            const int row = r0 + lane;
+                            int len = 0, klo = 0, ii = 0, jj = 0;
+                            double b2 = 0.0, dx = 0.0, dy = 0.0;
+                            if (row < rend) {
+                                ii = idiv(row, inv_nj);
+                                jj = row - ii * nj;
+                                dx = W.dx[ii];
+                                dy = W.dy[jj];
+                                b2 = fma(dy, dy, dx * dx);
+                                const double rem = dzr2 - b2;
+                                if (rem > 0.0) {
+                                    const float rho = fmaf(approx_sqrt((float)rem), 1.0001f,
+                                                           1e-5f * (float)dzr);
+                                    klo = max(0, __float2int_ru(fmaxf((dz0 - rho) * inv_res, -1.0f)));
+                                    const int khi = min(
+                                        nk - 1, __float2int_rd(fminf((dz0 + rho) * inv_res, (float)nk)));
+                                    len = max(0, khi - klo + 1);
+                                }
+                            }
+                            // inclusive scan of len
+                            int sc = len;
+#pragma unroll
+                            for (int o = 1; o < 32; o <<= 1) {
+                                const int t = __shfl_up_sync(0xffffffffu, sc, o);
+                                if (lane >= o) sc += t;
+                            }
+                            const unsigned m = __ballot_sync(0xffffffffu, len > 0);
+                            if (len > 0) {
+                                RowEntry &R = W.rows[nrow + __popc(m & lt)];
+                                R.start = total + sc - len;
+                                R.kpack = klo | (ii << 8) | (jj << 16);
+                                R.b2 = b2;
+                                R.exy = W.ex[ii] * W.ey[jj] * m4inv_r2;
+                                R.dx = dx;
+                                R.dy = dy;
+                            }
+                            nrow += __popc(m);
+                            total += __shfl_sync(0xffffffffu, sc, 31);
+                        }
+                        __syncwarp();
+                        // ---- phase 2: 4 windows of 32 voxels per step over the flattened
+                        // rows; all four loads are in flight before any is used ----
+                        int cur = 0;  // row containing the next window's first voxel
+                        for (int base = 0; base < total; base += 128) {
+                            int myrow[4];
+#pragma unroll
+                            for (int u = 0; u < 4; u++) {
+                                const int wb = base + 32 * u;
+                                // rows starting strictly inside the window (offsets 1..31)
+                                unsigned bits = 0u;
+                                bool at32 = false;
+                                const int q = cur + 1 + lane;
+                                if (q < nrow) {
+                                    const int off = W.rows[q].start - wb;
+                                    if (off > 0 && off < 32) bits = 1u << off;
+                                    at32 = off == 32;
+                                }
+                                const unsigned M = __reduce_or_sync(0xffffffffu, bits);
+                                myrow[u] = cur + __popc(M & ((lt << 1) | 1u));
+                                cur += __popc(M) + (__any_sync(0xffffffffu, at32) ? 1 : 0);
+                            }
+                            float g[4];
+                            int kk[4];
+#pragma unroll
+                            for (int u = 0; u < 4; u++) {
+                                const int v = base + 32 * u + lane;
+                                g[u] = 0.0f;
+                                kk[u] = 0;
+                                if (v < total) {
+                                    const int kp = W.rows[myrow[u]].kpack;
+                                    kk[u] = (kp & 0xff) + (v - W.rows[myrow[u]].start);
+                                    const int ii = (kp >> 8) & 0xff, jj = kp >> 16;
+                                    g[u] = __ldg(gsub + ((size_t)ii * D + jj) * D + kk[u]);
+                                }
+                            }
+#pragma unroll
+                            for (int u = 0; u < 4; u++) {
+                                const int v = base + 32 * u + lane;
+                                if (v < total) {
+                                    const RowEntry &R = W.rows[myrow[u]];
+                                    const double dz = W.dz[kk[u]];
+                                    const double d2 = fma(dz, dz, R.b2);
+                                    const bool in = d2 > 0.0 && d2 < dzr2;
+                                    const double gv = in ? widen(g[u]) : 0.0;
+                                    const double rd = rsqrt_d(d2);
+                                    const double sq = gv * qa2 * fma(-dzr, rd, 1.0);
+                                    const double sg = gv * (R.exy * W.ez[kk[u]]);
+                                    const double scl = d2 <= d02 ? sg : sq;
+                                    if (u & 1) {
+                                        gx1 = fma(scl, R.dx, gx1);
+                                        gy1 = fma(scl, R.dy, gy1);
+                                        gz1 = fma(scl, dz, gz1);
+                                    } else {
+                                        gx0 = fma(scl, R.dx, gx0);
+                                        gy0 = fma(scl, R.dy, gy0);
+                                        gz0 = fma(scl, dz, gz0);
+                                    }
+                                }
                             }
                         }
+                        __syncwarp();
                     }
-                    // the whole row span first (<= kSub loads in flight), then the math
-                    float g[kSub];
-#pragma unroll
-                    for (int q = 0; q < kSub; q++)
-                        g[q] = (klo + q <= khi) ? __ldg(gr + klo + q) : 0.0f;
-                    double cs = 0.0, csz = 0.0, ts = 0.0, tsz = 0.0;
-#pragma unroll
-                    for (int q = 0; q < kSub; q++) {
-                        const int kk = klo + q;
-                        if (kk > khi) break;
-                        const double gq = (double)g[q];
-                        if (kk >= kc0 && kk <= kc1) {
-                            cs = fma(gq, T.ez[kk], cs);
-                            csz = fma(gq, T.ezdz[kk], csz);
-                        } else {
-                            // shell and boundary voxels: exact f64 classification
-                            const double dz = T.dz[kk];
-                            const double d2 = fma(dz, dz, b2);
-                            const bool in = d2 > 0.0 && d2 < A.dzr2;
-                            const double gv = in ? gq : 0.0;
-                            const double rd = rsqrt_d(d2);
-                            const double sq = gv * qa2 * fma(-A.dzr, rd, 1.0);
-                            const double sg = gv * (exy * T.ez[kk]);
-                            const double sc = d2 <= d02 ? sg : sq;
-                            ts += sc;
-                            tsz = fma(sc, dz, tsz);
-                        }
-                    }
-                    // slope/d * offset summed over the row: core terms share exy
-                    const double srow = fma(exy, cs, ts);
-                    ax0 = fma(srow, dx, ax0);
-                    ay0 = fma(srow, dy, ay0);
-                    az0 = fma(exy, csz, az0 + tsz);
                 }
-            }
-    double gx = ax0 + ax1, gy = ay0 + ay1, gz = az0 + az1;
-#pragma unroll
-    for (int o = 1; o < kLPA; o <<= 1) {
-        gx += __shfl_xor_sync(0xffffffffu, gx, o);
-        gy += __shfl_xor_sync(0xffffffffu, gy, o);
-        gz += __shfl_xor_sync(0xffffffffu, gz, o);
     }
-    if (live && sub == 0) {
-        P.coord_grad[3 * a + 0] = (float)gx;
-        P.coord_grad[3 * a + 1] = (float)gy;
-        P.coord_grad[3 * a + 2] = (float)gz;
-    }
+    store_coord(P, a, lane, gx0 + gx1, gy0 + gy1, gz0 + gz1);
 }
 
 // Vector types (_kernels.py:258-314).  With per-atom radii and <= kMaxT
@@ -458,10 +532,16 @@ gm_status backward_impl(const gm_params *p, const gm_batch *b, const Workspace &
     P.grid_grad = grid_grad;
     P.coord_grad = coord_grad;
     P.type_grad = type_grad;
+    P.items = ws.items;
+    P.eg = exp((-2.0 * p->gaussian_radius_multiple) * p->gaussian_radius_multiple);
+    {
+        const char *d = getenv("GM_DEBUG_BWD");
+        P.dbg = d ? atoi(d) : 0;
+    }
     if (b->vector_mode)
         k_backward_vector<<<(b->natoms + kWarps - 1) / kWarps, 256, 0, s>>>(P);
     else
-        k_backward_index<<<(b->natoms + kAtomsPerBlock - 1) / kAtomsPerBlock, 256, 0, s>>>(P);
+        k_backward_index<<<(b->natoms + kBwdWarps - 1) / kBwdWarps, kBwdWarps * 32, 0, s>>>(P);
     LAUNCH_CHECK();
     return GM_OK;
 }
