@@ -231,7 +231,7 @@ struct WarpBwd {
     RowEntry rows[kRows];
 };
 
-__global__ void __launch_bounds__(kBwdWarps * 32) k_backward_index(const BwdArgs P) {
+__global__ void __launch_bounds__(kBwdWarps * 32, 6) k_backward_index(const BwdArgs P) {
     __shared__ WarpBwd wsm[kBwdWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int a = blockIdx.x * kBwdWarps + warp;

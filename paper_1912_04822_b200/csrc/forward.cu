@@ -24,7 +24,7 @@
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 128;
 constexpr int kWarps = kThreads / 32;
 
 struct FwdArgs {
@@ -129,7 +129,7 @@ __device__ __forceinline__ bool plan_visit(const FwdItem &it, int i, int jg0, in
 }
 
 template <bool BINARY, bool VECTOR, bool RESL>
-__global__ void __launch_bounds__(kThreads, 2) k_forward(const FwdArgs A) {
+__global__ void __launch_bounds__(kThreads, 5) k_forward(const FwdArgs A) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int c = blockIdx.x % A.C, tile = blockIdx.x / A.C, e = blockIdx.y;
@@ -321,10 +321,10 @@ struct FwdConfig {
 };
 
 FwdConfig choose_config(int D) {
-    const size_t budget = 80 * 1024;  // acc; + 16 KB of slots -> 2 CTAs per SM
+    const size_t budget = 37 * 1024;  // acc; + 8 KB of slots -> 5 CTAs per SM
     const size_t plane = (size_t)D * D * 4;
     FwdConfig cfg{};
-    int TI = 8;
+    int TI = kWarps;
     while (TI > 1 && (TI * plane > budget || TI > D)) TI >>= 1;
     cfg.TI = TI;
     cfg.wpp = kWarps / TI;
