@@ -186,20 +186,32 @@ __global__ void __launch_bounds__(kThreads, 5) k_forward(const FwdArgs A) {
         const float resf = A.resf, resl = A.resl, inv_res = A.inv_res;
         const double ox = A.origins[3 * e + 0], oy = A.origins[3 * e + 1],
                      oz = A.origins[3 * e + 2];
+        // the next chunk's records are prefetched into registers while the
+        // current chunk scatters (hides the L2 latency of phase A)
+        FwdItem nxt;
+        int2 nbox = make_int2(1, 0);  // empty box
+        if (cs + lane < ce) {
+            nbox = A.sbox[cs + lane];
+            nxt = A.sorted[cs + lane];
+        }
         for (int base = cs; base < ce; base += 32) {
             // ---- phase A: lane t plans item base + t ----
             const int it = base + lane;
+            const FwdItem cur_item = nxt;
+            const int2 bx = nbox;
+            nbox = make_int2(1, 0);
+            if (it + 32 < ce) {
+                nbox = A.sbox[it + 32];
+                nxt = A.sorted[it + 32];
+            }
             bool hit = false;
-            if (it < ce) {
-                const int2 bx = A.sbox[it];
-                if (box_lo(bx.x) <= i && box_hi(bx.x) >= i && box_lo(bx.y) <= jg1 &&
-                    box_hi(bx.y) >= jg0) {
-                    Slot S;
-                    hit = plan_visit(A.sorted[it], i, jg0, jg1, j0, D, resf, resl, inv_res, S);
-                    if (hit) {
-                        S.src = it;
-                        slots[lane] = S;
-                    }
+            if (it < ce && box_lo(bx.x) <= i && box_hi(bx.x) >= i && box_lo(bx.y) <= jg1 &&
+                box_hi(bx.y) >= jg0) {
+                Slot S;
+                hit = plan_visit(cur_item, i, jg0, jg1, j0, D, resf, resl, inv_res, S);
+                if (hit) {
+                    S.src = it;
+                    slots[lane] = S;
                 }
             }
             unsigned m = __ballot_sync(0xffffffffu, hit);
