@@ -22,9 +22,7 @@
 
 namespace {
 
-constexpr int kMaxN = 32;   // table entries per axis (sub-box edge)
 constexpr int kMaxT = 16;   // channels kept in registers by the shared-geometry vector path
-constexpr int kWarps = 8;
 
 struct BwdArgs {
     gm_params p;
@@ -38,9 +36,6 @@ struct BwdArgs {
     int dbg;
 };
 
-struct Tables {
-    double dx[kMaxN], ex[kMaxN], dy[kMaxN], ey[kMaxN], dz[kMaxN], ez[kMaxN];
-};
 
 // One atom (for one channel radius): position, origin, full voxel box.
 struct Atom {
@@ -92,81 +87,6 @@ __device__ __forceinline__ int idiv(int a, float inv_b) {
     return (int)(((float)a + 0.5f) * inv_b);
 }
 
-// Walk the box of atom A (cutoff A.dzr) over grid channel gbase.  For every
-// voxel with d2 < dzr2 (and d2 > 0 when SKIP_CENTER) -- and, when LOAD,
-// g != 0 -- calls f(slot, d2, dx, dy, dz, Exyz, g_or_voxel_offset) in a fixed
-// order per lane.  Lanes own (i, j) rows of the box; a row visits only the k
-// span inside the cutoff sphere, four voxels at a time (loads first).  With
-// LOAD the walk passes g; otherwise the voxel offset (as double) and the
-// callee loads.  `slot` alternates between two accumulator chains.
-template <bool SKIP_CENTER, bool LOAD, typename F>
-__device__ __forceinline__ void walk(const Atom &A, Tables &T, const float *gbase, int D,
-                                     double res, float inv_res, int lane, F &&f) {
-    for (int si = A.i0; si <= A.i1; si += kMaxN)
-        for (int sj = A.j0; sj <= A.j1; sj += kMaxN)
-            for (int sk = A.k0; sk <= A.k1; sk += kMaxN) {
-                const int ni = min(kMaxN, A.i1 - si + 1), nj = min(kMaxN, A.j1 - sj + 1),
-                          nk = min(kMaxN, A.k1 - sk + 1);
-                __syncwarp();
-                if (lane < ni) {
-                    const double d = offs(A.x, A.ox, si + lane, res);
-                    T.dx[lane] = d;
-                    T.ex[lane] = exp(A.m2inv_r2 * (d * d));
-                }
-                if (lane < nj) {
-                    const double d = offs(A.y, A.oy, sj + lane, res);
-                    T.dy[lane] = d;
-                    T.ey[lane] = exp(A.m2inv_r2 * (d * d));
-                }
-                if (lane < nk) {
-                    const double d = offs(A.z, A.oz, sk + lane, res);
-                    T.dz[lane] = d;
-                    T.ez[lane] = exp(A.m2inv_r2 * (d * d));
-                }
-                __syncwarp();
-                const float inv_nj = __frcp_rn((float)nj);
-                const float dz0 = (float)T.dz[0];
-                const int nrows = ni * nj;
-                for (int row = lane; row < nrows; row += 32) {
-                    const int ii = idiv(row, inv_nj), jj = row - ii * nj;
-                    const double dx = T.dx[ii], dy = T.dy[jj];
-                    const double b2 = fma(dy, dy, dx * dx);
-                    const double rem = A.dzr2 - b2;
-                    if (rem <= 0.0) continue;  // the whole row is at or beyond the cutoff
-                    const float rho = fmaf(sqrtf((float)rem), 1.0001f, 1e-5f * (float)A.dzr);
-                    const int klo = max(0, (int)ceilf(fmaxf((dz0 - rho) * inv_res, -1.0f)));
-                    const int khi = min(nk - 1, (int)floorf(fminf((dz0 + rho) * inv_res, (float)nk)));
-                    const double exy = T.ex[ii] * T.ey[jj];
-                    const size_t rbase = ((size_t)(si + ii) * D + (sj + jj)) * D + sk;
-                    for (int k0 = klo; k0 <= khi; k0 += 4) {
-                        float g[4];
-                        double d2[4];
-#pragma unroll
-                        for (int u = 0; u < 4; u++) {
-                            const int kk = k0 + u;
-                            bool in = false;
-                            d2[u] = A.dzr2;
-                            if (kk <= khi) {
-                                const double dz = T.dz[kk];
-                                d2[u] = fma(dz, dz, b2);
-                                in = (SKIP_CENTER ? d2[u] > 0.0 : true) && d2[u] < A.dzr2;
-                            }
-                            if (LOAD) g[u] = in ? __ldg(gbase + rbase + kk) : 0.0f;
-                            else g[u] = in ? 1.0f : 0.0f;
-                        }
-#pragma unroll
-                        for (int u = 0; u < 4; u++) {
-                            if (g[u] != 0.0f) {
-                                const int kk = k0 + u;
-                                const double gv = LOAD ? (double)g[u] : (double)(rbase + kk);
-                                f(u & 1, d2[u], dx, dy, T.dz[kk], exy * T.ez[kk], gv);
-                            }
-                        }
-                    }
-                }
-            }
-}
-
 __device__ __forceinline__ void load_atom(const BwdArgs &P, int a, Atom &A, int &s, int &e) {
     const gm_batch &b = P.b;
     s = b.atom_set[a];
@@ -203,26 +123,28 @@ __device__ __forceinline__ void store_coord(const BwdArgs &P, int a, int lane, d
 }
 
 // ---------------------------------------------------------------------------
-// Index types: one warp per atom, flattened walk.
+// One warp per atom, flattened walk (index and vector types).
 //
-// The atom's box is cut into chunks of <= kRows (i, j) rows.  Phase 1: lanes
-// compute each row's k span inside the cutoff sphere and a warp scan lays the
-// non-empty rows out back to back (row table in shared memory: start offset,
-// k origin, b2 = dx^2 + dy^2, dx, dy, Gaussian factor).  Phase 2: the warp
-// walks the flattened list 32 voxels at a time -- every lane has a voxel, so
-// no lane idles on short rows; a lane finds its row from a bit mask of the
-// row starts inside the window (REDUX + popc).  Geometry and accumulation in
+// The atom's box is cut into sub-boxes of <= kTab voxels per axis and chunks
+// of <= kRows (i, j) rows.  Phase 1: lanes compute each row's k span inside
+// the cutoff sphere and a warp scan lays the non-empty rows out back to back
+// (row table in shared memory: start offset, k origin, b2 = dx^2 + dy^2, dx,
+// dy, Gaussian factor Ex*Ey).  Phase 2: the warp walks the flattened list in
+// windows of 32 voxels, kU windows per step -- every lane has a voxel (no
+// lane idles on short rows); a lane finds its row from a bit mask of the row
+// starts inside its window (REDUX + popc).  Geometry and accumulation in
 // f64; the tail's 1/d from MUFU.RSQ64H + one Newton step.
 // ---------------------------------------------------------------------------
 constexpr int kBwdWarps = 4;
 constexpr int kRows = 96;     // rows per chunk
 constexpr int kTab = 32;      // table entries per axis (sub-box edge)
+constexpr int kU = 4;         // 32-voxel windows per step (loads in flight per lane)
 
 struct __align__(16) RowEntry {
     int start;   // offset of the row's first voxel in the flattened list
     int kpack;   // k0 (relative to the sub-box) | (i_rel << 8) | (j_rel << 16)
     double b2;   // dx^2 + dy^2
-    double exy;  // Ex * Ey * (-4 / r^2)
+    double exy;  // Ex * Ey
     double dx, dy;
 };
 
@@ -231,13 +153,138 @@ struct WarpBwd {
     RowEntry rows[kRows];
 };
 
+// f(slot, d2, R, dz, ez, voxel_offset, g): every voxel of the box with
+// d2 < dzr2 (others get g = 0 / are skipped), g loaded by the walk when LOADG.
+template <bool LOADG, typename F>
+__device__ __forceinline__ void flat_walk(const Atom &A, WarpBwd &W, const float *gbase, int D,
+                                          double res, float inv_res, int lane, F &&f) {
+    const unsigned lt = (1u << lane) - 1u;
+    const double dzr = A.dzr, dzr2 = A.dzr2;
+    for (int si = A.i0; si <= A.i1; si += kTab)
+        for (int sj = A.j0; sj <= A.j1; sj += kTab)
+            for (int sk = A.k0; sk <= A.k1; sk += kTab) {
+                const int ni = min(kTab, A.i1 - si + 1), nj = min(kTab, A.j1 - sj + 1),
+                          nk = min(kTab, A.k1 - sk + 1);
+                __syncwarp();
+                for (int l = lane; l < ni + nj + nk; l += 32) {
+                    const int ax = l < ni ? 0 : (l < ni + nj ? 1 : 2);
+                    const int q = l - (ax == 0 ? 0 : (ax == 1 ? ni : ni + nj));
+                    const double d = ax == 0 ? offs(A.x, A.ox, si + q, res)
+                                             : (ax == 1 ? offs(A.y, A.oy, sj + q, res)
+                                                        : offs(A.z, A.oz, sk + q, res));
+                    const double E = exp(A.m2inv_r2 * (d * d));
+                    double *dt = ax == 0 ? W.dx : (ax == 1 ? W.dy : W.dz);
+                    double *et = ax == 0 ? W.ex : (ax == 1 ? W.ey : W.ez);
+                    dt[q] = d;
+                    et[q] = E;
+                }
+                __syncwarp();
+                const float dz0 = (float)W.dz[0];
+                const float inv_nj = __frcp_rn((float)nj);
+                const size_t sbase = ((size_t)si * D + sj) * D + sk;
+                const int nrows_all = ni * nj;
+                for (int rb = 0; rb < nrows_all; rb += kRows) {
+                    // ---- phase 1: row spans, compacted with a warp scan ----
+                    int nrow = 0, total = 0;
+                    const int rend = min(nrows_all, rb + kRows);
+                    for (int r0 = rb; r0 < rend; r0 += 32) {
+                        const int row = r0 + lane;
+                        int len = 0, klo = 0, ii = 0, jj = 0;
+                        double b2 = 0.0, dx = 0.0, dy = 0.0;
+                        if (row < rend) {
+                            ii = idiv(row, inv_nj);
+                            jj = row - ii * nj;
+                            dx = W.dx[ii];
+                            dy = W.dy[jj];
+                            b2 = fma(dy, dy, dx * dx);
+                            const double rem = dzr2 - b2;
+                            if (rem > 0.0) {
+                                const float rho =
+                                    fmaf(approx_sqrt((float)rem), 1.0001f, 1e-5f * (float)dzr);
+                                klo = max(0, __float2int_ru(fmaxf((dz0 - rho) * inv_res, -1.0f)));
+                                const int khi = min(
+                                    nk - 1, __float2int_rd(fminf((dz0 + rho) * inv_res, (float)nk)));
+                                len = max(0, khi - klo + 1);
+                            }
+                        }
+                        int sc = len;  // inclusive scan of the span lengths
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int t = __shfl_up_sync(0xffffffffu, sc, o);
+                            if (lane >= o) sc += t;
+                        }
+                        const unsigned m = __ballot_sync(0xffffffffu, len > 0);
+                        if (len > 0) {
+                            RowEntry &R = W.rows[nrow + __popc(m & lt)];
+                            R.start = total + sc - len;
+                            R.kpack = klo | (ii << 8) | (jj << 16);
+                            R.b2 = b2;
+                            R.exy = W.ex[ii] * W.ey[jj];
+                            R.dx = dx;
+                            R.dy = dy;
+                        }
+                        nrow += __popc(m);
+                        total += __shfl_sync(0xffffffffu, sc, 31);
+                    }
+                    __syncwarp();
+                    // ---- phase 2: kU windows of 32 voxels per step ----
+                    int cur = 0;  // row containing the next window's first voxel
+                    for (int base = 0; base < total; base += 32 * kU) {
+                        int myrow[kU];
+#pragma unroll
+                        for (int u = 0; u < kU; u++) {
+                            const int wb = base + 32 * u;
+                            unsigned bits = 0u;  // rows starting at window offsets 1..31
+                            bool at32 = false;
+                            const int q = cur + 1 + lane;
+                            if (q < nrow) {
+                                const int off = W.rows[q].start - wb;
+                                if (off > 0 && off < 32) bits = 1u << off;
+                                at32 = off == 32;
+                            }
+                            const unsigned M = __reduce_or_sync(0xffffffffu, bits);
+                            myrow[u] = cur + __popc(M & ((lt << 1) | 1u));
+                            cur += __popc(M) + (__any_sync(0xffffffffu, at32) ? 1 : 0);
+                        }
+                        float g[kU];
+                        int kk[kU];
+                        size_t vo[kU];
+#pragma unroll
+                        for (int u = 0; u < kU; u++) {
+                            const int v = base + 32 * u + lane;
+                            g[u] = 0.0f;
+                            kk[u] = 0;
+                            vo[u] = 0;
+                            if (v < total) {
+                                const int kp = W.rows[myrow[u]].kpack;
+                                kk[u] = (kp & 0xff) + (v - W.rows[myrow[u]].start);
+                                const int ii = (kp >> 8) & 0xff, jj = kp >> 16;
+                                vo[u] = sbase + ((size_t)ii * D + jj) * D + kk[u];
+                                if (LOADG) g[u] = __ldg(gbase + vo[u]);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < kU; u++) {
+                            const int v = base + 32 * u + lane;
+                            if (v < total) {
+                                const RowEntry &R = W.rows[myrow[u]];
+                                const double dz = W.dz[kk[u]];
+                                const double d2 = fma(dz, dz, R.b2);
+                                f(u & 1, d2, R, dz, W.ez[kk[u]], vo[u], g[u]);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+}
+
 __global__ void __launch_bounds__(kBwdWarps * 32, 6) k_backward_index(const BwdArgs P) {
     __shared__ WarpBwd wsm[kBwdWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int a = blockIdx.x * kBwdWarps + warp;
     const gm_batch &b = P.b;
     if (a >= b.natoms) return;
-    WarpBwd &W = wsm[warp];
     const int D = P.p.npts;
     const double res = P.p.resolution, grm = P.p.gaussian_radius_multiple;
     const float inv_res = (float)(1.0 / res);
@@ -250,8 +297,6 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 6) k_backward_index(const BwdA
     const double q0 = (2.0 * grm) / r;
     const double qa2 = 2.0 * (P.eg * (q0 * q0));
     const double m4inv_r2 = -4.0 / (r * r);
-    double gx0 = 0.0, gy0 = 0.0, gz0 = 0.0, gx1 = 0.0, gy1 = 0.0, gz1 = 0.0;
-    const unsigned lt = (1u << lane) - 1u;
     // the forward item of this atom carries the same box (_kernels.py:225-227)
     const int4 bx = *reinterpret_cast<const int4 *>(&P.items[a].ibox);
     A.dzr = P.p.radius_multiple * r;
@@ -263,154 +308,43 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 6) k_backward_index(const BwdA
     A.j1 = box_hi(bx.y);
     A.k0 = box_lo(bx.z);
     A.k1 = box_hi(bx.z);
-    (void)D;
+    double g0x = 0.0, g0y = 0.0, g0z = 0.0, g1x = 0.0, g1y = 0.0, g1z = 0.0;
     if (A.i0 <= A.i1 && A.j0 <= A.j1 && A.k0 <= A.k1) {
-        const size_t D3 = (size_t)D * D * D;
-        const float *gbase = P.grid_grad + ((size_t)e * b.nchannels + c) * D3;
+        const float *gbase = P.grid_grad + ((size_t)e * b.nchannels + c) * ((size_t)D * D * D);
         const double dzr = A.dzr, dzr2 = A.dzr2;
-        for (int si = A.i0; si <= A.i1; si += kTab)
-            for (int sj = A.j0; sj <= A.j1; sj += kTab)
-                for (int sk = A.k0; sk <= A.k1; sk += kTab) {
-                    const int ni = min(kTab, A.i1 - si + 1), nj = min(kTab, A.j1 - sj + 1),
-                              nk = min(kTab, A.k1 - sk + 1);
-                    __syncwarp();
-                    for (int l = lane; l < ni + nj + nk; l += 32) {
-                        const int ax = l < ni ? 0 : (l < ni + nj ? 1 : 2);
-                        const int q = l - (ax == 0 ? 0 : (ax == 1 ? ni : ni + nj));
-                        const double d = ax == 0 ? offs(A.x, A.ox, si + q, res)
-                                                 : (ax == 1 ? offs(A.y, A.oy, sj + q, res)
-                                                            : offs(A.z, A.oz, sk + q, res));
-                        const double E = exp(A.m2inv_r2 * (d * d));
-                        double *dt = ax == 0 ? W.dx : (ax == 1 ? W.dy : W.dz);
-                        double *et = ax == 0 ? W.ex : (ax == 1 ? W.ey : W.ez);
-                        dt[q] = d;
-                        et[q] = E;
-                    }
-                    __syncwarp();
-                    const float dz0 = (float)W.dz[0];
-                    const float inv_nj = __frcp_rn((float)nj);
-                    const float *gsub = gbase + ((size_t)si * D + sj) * D + sk;
-                    const int nrows_all = ni * nj;
-                    for (int rb = 0; rb < nrows_all; rb += kRows) {
-                        // ---- phase 1: row spans, compacted with a warp scan ----
-                        int nrow = 0, total = 0;
-                        const int rend = min(nrows_all, rb + kRows);
-                        for (int r0 = rb; r0 < rend; r0 += 32) {
-                            const int row = r0 + lane;
-                            int len = 0, klo = 0, ii = 0, jj = 0;
-                            double b2 = 0.0, dx = 0.0, dy = 0.0;
-                            if (row < rend) {
-                                ii = idiv(row, inv_nj);
-                                jj = row - ii * nj;
-                                dx = W.dx[ii];
-                                dy = W.dy[jj];
-                                b2 = fma(dy, dy, dx * dx);
-                                const double rem = dzr2 - b2;
-                                if (rem > 0.0) {
-                                    const float rho = fmaf(approx_sqrt((float)rem), 1.0001f,
-                                                           1e-5f * (float)dzr);
-                                    klo = max(0, __float2int_ru(fmaxf((dz0 - rho) * inv_res, -1.0f)));
-                                    const int khi = min(
-                                        nk - 1, __float2int_rd(fminf((dz0 + rho) * inv_res, (float)nk)));
-                                    len = max(0, khi - klo + 1);
-                                }
+        flat_walk<true>(A, wsm[warp], gbase, D, res, inv_res, lane,
+                        [&](int slot, double d2, const RowEntry &R, double dz, double ez, size_t,
+                            float g) {
+                            // slope/d: Gaussian exp(-2d^2/r^2)(-4/r^2) (separable factors);
+                            // tail 2 qa (d - dzr) / d (_kernels.py:244-251)
+                            const bool in = d2 > 0.0 && d2 < dzr2;
+                            const double gv = in ? widen(g) : 0.0;
+                            const double rd = rsqrt_d(d2);
+                            const double sq = gv * qa2 * fma(-dzr, rd, 1.0);
+                            const double sg = gv * (R.exy * ez) * m4inv_r2;
+                            const double scl = d2 <= d02 ? sg : sq;
+                            if (slot) {
+                                g1x = fma(scl, R.dx, g1x);
+                                g1y = fma(scl, R.dy, g1y);
+                                g1z = fma(scl, dz, g1z);
+                            } else {
+                                g0x = fma(scl, R.dx, g0x);
+                                g0y = fma(scl, R.dy, g0y);
+                                g0z = fma(scl, dz, g0z);
                             }
-                            // inclusive scan of len
-                            int sc = len;
-#pragma unroll
-                            for (int o = 1; o < 32; o <<= 1) {
-                                const int t = __shfl_up_sync(0xffffffffu, sc, o);
-                                if (lane >= o) sc += t;
-                            }
-                            const unsigned m = __ballot_sync(0xffffffffu, len > 0);
-                            if (len > 0) {
-                                RowEntry &R = W.rows[nrow + __popc(m & lt)];
-                                R.start = total + sc - len;
-                                R.kpack = klo | (ii << 8) | (jj << 16);
-                                R.b2 = b2;
-                                R.exy = W.ex[ii] * W.ey[jj] * m4inv_r2;
-                                R.dx = dx;
-                                R.dy = dy;
-                            }
-                            nrow += __popc(m);
-                            total += __shfl_sync(0xffffffffu, sc, 31);
-                        }
-                        __syncwarp();
-                        // ---- phase 2: 4 windows of 32 voxels per step over the flattened
-                        // rows; all four loads are in flight before any is used ----
-                        int cur = 0;  // row containing the next window's first voxel
-                        for (int base = 0; base < total; base += 128) {
-                            int myrow[4];
-#pragma unroll
-                            for (int u = 0; u < 4; u++) {
-                                const int wb = base + 32 * u;
-                                // rows starting strictly inside the window (offsets 1..31)
-                                unsigned bits = 0u;
-                                bool at32 = false;
-                                const int q = cur + 1 + lane;
-                                if (q < nrow) {
-                                    const int off = W.rows[q].start - wb;
-                                    if (off > 0 && off < 32) bits = 1u << off;
-                                    at32 = off == 32;
-                                }
-                                const unsigned M = __reduce_or_sync(0xffffffffu, bits);
-                                myrow[u] = cur + __popc(M & ((lt << 1) | 1u));
-                                cur += __popc(M) + (__any_sync(0xffffffffu, at32) ? 1 : 0);
-                            }
-                            float g[4];
-                            int kk[4];
-#pragma unroll
-                            for (int u = 0; u < 4; u++) {
-                                const int v = base + 32 * u + lane;
-                                g[u] = 0.0f;
-                                kk[u] = 0;
-                                if (v < total) {
-                                    const int kp = W.rows[myrow[u]].kpack;
-                                    kk[u] = (kp & 0xff) + (v - W.rows[myrow[u]].start);
-                                    const int ii = (kp >> 8) & 0xff, jj = kp >> 16;
-                                    g[u] = __ldg(gsub + ((size_t)ii * D + jj) * D + kk[u]);
-                                }
-                            }
-#pragma unroll
-                            for (int u = 0; u < 4; u++) {
-                                const int v = base + 32 * u + lane;
-                                if (v < total) {
-                                    const RowEntry &R = W.rows[myrow[u]];
-                                    const double dz = W.dz[kk[u]];
-                                    const double d2 = fma(dz, dz, R.b2);
-                                    const bool in = d2 > 0.0 && d2 < dzr2;
-                                    const double gv = in ? widen(g[u]) : 0.0;
-                                    const double rd = rsqrt_d(d2);
-                                    const double sq = gv * qa2 * fma(-dzr, rd, 1.0);
-                                    const double sg = gv * (R.exy * W.ez[kk[u]]);
-                                    const double scl = d2 <= d02 ? sg : sq;
-                                    if (u & 1) {
-                                        gx1 = fma(scl, R.dx, gx1);
-                                        gy1 = fma(scl, R.dy, gy1);
-                                        gz1 = fma(scl, dz, gz1);
-                                    } else {
-                                        gx0 = fma(scl, R.dx, gx0);
-                                        gy0 = fma(scl, R.dy, gy0);
-                                        gz0 = fma(scl, dz, gz0);
-                                    }
-                                }
-                            }
-                        }
-                        __syncwarp();
-                    }
-                }
+                        });
     }
-    store_coord(P, a, lane, gx0 + gx1, gy0 + gy1, gz0 + gz1);
+    store_coord(P, a, lane, g0x + g1x, g0y + g1y, g0z + g1z);
 }
 
 // Vector types (_kernels.py:258-314).  With per-atom radii and <= kMaxT
 // channels the geometry is shared by all channels of the set: one walk, all
 // channel gradients per voxel, the coordinate term from sum_c w_c g_c.  With
 // type-indexed radii (or more channels) each channel walks its own box.
-__global__ void __launch_bounds__(256) k_backward_vector(const BwdArgs P) {
-    __shared__ Tables tabs[kWarps];
+__global__ void __launch_bounds__(kBwdWarps * 32) k_backward_vector(const BwdArgs P) {
+    __shared__ WarpBwd wsm[kBwdWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int a = blockIdx.x * kWarps + warp;
+    const int a = blockIdx.x * kBwdWarps + warp;
     const gm_batch &b = P.b;
     if (a >= b.natoms) return;
     const int D = P.p.npts;
@@ -423,7 +357,6 @@ __global__ void __launch_bounds__(256) k_backward_vector(const BwdArgs P) {
     const int Tn = b.set_t[s];
     const int row = b.set_wstart[s] + (a - b.set_start[s]) * Tn;
     const size_t D3 = (size_t)D * D * D;
-    const double eg = exp((-2.0 * grm) * grm);
     const float *gset = P.grid_grad + ((size_t)e * b.nchannels + b.set_choff[s]) * D3;
     double gx = 0.0, gy = 0.0, gz = 0.0;
 
@@ -431,7 +364,7 @@ __global__ void __launch_bounds__(256) k_backward_vector(const BwdArgs P) {
         const double r = b.atom_radius[a];
         const double gr = grm * r, d02 = gr * gr;
         const double q0 = (2.0 * grm) / r;
-        const double qa = eg * (q0 * q0);
+        const double qa = P.eg * (q0 * q0);
         const double m4inv_r2 = -4.0 / (r * r);
         double w[kMaxT], tg[kMaxT];
 #pragma unroll
@@ -440,37 +373,42 @@ __global__ void __launch_bounds__(256) k_backward_vector(const BwdArgs P) {
             tg[c] = 0.0;
         }
         if (set_radius(A, r, rmult, res, D)) {
-            const double dzr = A.dzr;
-            walk<false, false>(A, tabs[warp], gset, D, res, inv_res, lane,
-                               [&](int, double d2, double dx, double dy, double dz, double exyz,
-                                   double voff) {
-                                   double dens, sod;  // density, slope / d
-                                   if (d2 <= d02) {
-                                       dens = exyz;
-                                       sod = dens * m4inv_r2;
-                                   } else {
-                                       const double rd = rsqrt_d(d2);
-                                       const double t = fma(d2, rd, -dzr);
-                                       dens = (qa * t) * t;
-                                       sod = (2.0 * qa) * t * rd;
-                                   }
-                                   const float *gv = gset + (size_t)voff;
-                                   double sw = 0.0;
+            const double dzr = A.dzr, dzr2 = A.dzr2;
+            flat_walk<false>(A, wsm[warp], gset, D, res, inv_res, lane,
+                             [&](int, double d2, const RowEntry &R, double dz, double ez,
+                                 size_t voff, float) {
+                                 if (d2 >= dzr2) return;
+                                 double dens, sod;  // density, slope / d
+                                 if (d2 <= d02) {
+                                     dens = R.exy * ez;
+                                     sod = dens * m4inv_r2;
+                                 } else {
+                                     const double rd = rsqrt_d(d2);
+                                     const double t = fma(d2, rd, -dzr);
+                                     dens = (qa * t) * t;
+                                     sod = (2.0 * qa) * t * rd;
+                                 }
+                                 const float *gv = gset + voff;
+                                 float gc[kMaxT];
 #pragma unroll
-                                   for (int c = 0; c < kMaxT; c++) {
-                                       if (c < Tn) {
-                                           const double g = (double)__ldg(gv + c * D3);
-                                           tg[c] = fma(g, dens, tg[c]);
-                                           sw = fma(w[c], g, sw);
-                                       }
-                                   }
-                                   if (d2 > 0.0) {
-                                       const double sc = sw * sod;
-                                       gx = fma(sc, dx, gx);
-                                       gy = fma(sc, dy, gy);
-                                       gz = fma(sc, dz, gz);
-                                   }
-                               });
+                                 for (int c = 0; c < kMaxT; c++)
+                                     gc[c] = c < Tn ? __ldg(gv + c * D3) : 0.0f;
+                                 double sw = 0.0;
+#pragma unroll
+                                 for (int c = 0; c < kMaxT; c++) {
+                                     if (c < Tn) {
+                                         const double g = widen(gc[c]);
+                                         tg[c] = fma(g, dens, tg[c]);
+                                         sw = fma(w[c], g, sw);
+                                     }
+                                 }
+                                 if (d2 > 0.0) {
+                                     const double sc = sw * sod;
+                                     gx = fma(sc, R.dx, gx);
+                                     gy = fma(sc, R.dy, gy);
+                                     gz = fma(sc, dz, gz);
+                                 }
+                             });
         }
 #pragma unroll
         for (int c = 0; c < kMaxT; c++) {
@@ -486,32 +424,34 @@ __global__ void __launch_bounds__(256) k_backward_vector(const BwdArgs P) {
             const double w = (double)b.weights[row + c];
             const double gr = grm * r, d02 = gr * gr;
             const double q0 = (2.0 * grm) / r;
-            const double qa = eg * (q0 * q0);
+            const double qa = P.eg * (q0 * q0);
             const double m4inv_r2 = -4.0 / (r * r);
             double tg = 0.0;
             if (set_radius(A, r, rmult, res, D)) {
-                const double dzr = A.dzr;
-                walk<false, true>(A, tabs[warp], gset + (size_t)c * D3, D, res, inv_res, lane,
-                                  [&](int, double d2, double dx, double dy, double dz, double exyz,
-                                      double g) {
-                                      double dens, sod;
-                                      if (d2 <= d02) {
-                                          dens = exyz;
-                                          sod = dens * m4inv_r2;
-                                      } else {
-                                          const double rd = rsqrt_d(d2);
-                                          const double t = fma(d2, rd, -dzr);
-                                          dens = (qa * t) * t;
-                                          sod = (2.0 * qa) * t * rd;
-                                      }
-                                      tg = fma(g, dens, tg);
-                                      if (d2 > 0.0 && w != 0.0) {
-                                          const double sc = (w * g) * sod;
-                                          gx = fma(sc, dx, gx);
-                                          gy = fma(sc, dy, gy);
-                                          gz = fma(sc, dz, gz);
-                                      }
-                                  });
+                const double dzr = A.dzr, dzr2 = A.dzr2;
+                flat_walk<true>(A, wsm[warp], gset + (size_t)c * D3, D, res, inv_res, lane,
+                                [&](int, double d2, const RowEntry &R, double dz, double ez,
+                                    size_t, float gf) {
+                                    if (d2 >= dzr2 || gf == 0.0f) return;
+                                    const double g = widen(gf);
+                                    double dens, sod;
+                                    if (d2 <= d02) {
+                                        dens = R.exy * ez;
+                                        sod = dens * m4inv_r2;
+                                    } else {
+                                        const double rd = rsqrt_d(d2);
+                                        const double t = fma(d2, rd, -dzr);
+                                        dens = (qa * t) * t;
+                                        sod = (2.0 * qa) * t * rd;
+                                    }
+                                    tg = fma(g, dens, tg);
+                                    if (d2 > 0.0 && w != 0.0) {
+                                        const double sc = (w * g) * sod;
+                                        gx = fma(sc, R.dx, gx);
+                                        gy = fma(sc, R.dy, gy);
+                                        gz = fma(sc, dz, gz);
+                                    }
+                                });
             }
             tg = warp_sum(tg);
             if (lane == 0 && P.type_grad) P.type_grad[row + c] = (float)tg;
@@ -539,7 +479,7 @@ gm_status backward_impl(const gm_params *p, const gm_batch *b, const Workspace &
         P.dbg = d ? atoi(d) : 0;
     }
     if (b->vector_mode)
-        k_backward_vector<<<(b->natoms + kWarps - 1) / kWarps, 256, 0, s>>>(P);
+        k_backward_vector<<<(b->natoms + kBwdWarps - 1) / kBwdWarps, kBwdWarps * 32, 0, s>>>(P);
     else
         k_backward_index<<<(b->natoms + kBwdWarps - 1) / kBwdWarps, kBwdWarps * 32, 0, s>>>(P);
     LAUNCH_CHECK();
