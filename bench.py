@@ -62,66 +62,76 @@ def load_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-class ClockSampler:
-    """SM clocks and throttle reasons sampled by NVML in a background thread
-    while the timed region runs (nvidia-smi's 100 ms minimum interval is
-    longer than a short timed region)."""
+_CLOCK_PROBE = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+print("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
+while True:
+    try:
+        print(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+              pynvml.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)
+    except Exception:
+        break
+    time.sleep(0.002)
+"""
 
-    # nvmlClocksEventReason* bits
+
+class ClockSampler:
+    """SM clocks and throttle reasons sampled by NVML during the timed region,
+    in a separate process (a sampling thread would steal the GIL from the
+    launch loop and open gaps on the device)."""
+
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
-        self.reasons = set()
-        self.max_mhz = None
-        self._stop = threading.Event()
-        self.thread = None
+        self.proc = None
 
     def start(self):
-        try:
-            import pynvml
-
-            pynvml.nvmlInit()
-            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-            idx = self.index
-            if vis:
-                try:
-                    idx = int(vis.split(",")[self.index])
-                except ValueError:
-                    idx = self.index
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-            self.nvml = pynvml
-        except Exception:
-            self.h = None
-            return
-        self.thread = threading.Thread(target=self._run, daemon=True)
-        self.thread.start()
-
-    def _run(self):
-        nv = self.nvml
-        while not self._stop.is_set():
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        idx = self.index
+        if vis:
             try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for b, name in self.REASONS.items():
-                    if bits & b:
-                        self.reasons.add(name)
-            except Exception:
-                break
-            time.sleep(0.002)
+                idx = int(vis.split(",")[self.index])
+            except ValueError:
+                idx = self.index
+        try:
+            self.proc = subprocess.Popen([sys.executable, "-c", _CLOCK_PROBE, str(idx)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
+            first = self.proc.stdout.readline().split()  # wait until NVML is up
+            self.max_mhz = float(first[1]) if len(first) == 2 else None
+        except Exception:
+            self.proc = None
 
     def stop(self):
-        if self.thread is None:
+        if self.proc is None:
             return None
-        self._stop.set()
-        self.thread.join(timeout=2)
-        if not self.samples:
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, reasons = [], set()
+        for ln in out.splitlines():
+            parts = ln.split()
+            if len(parts) != 2:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                bits = int(parts[1])
+            except ValueError:
+                continue
+            for b, name in self.REASONS.items():
+                if bits & b:
+                    reasons.add(name)
+        if not sm:
             return None
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(sm)}
 
 
 def dist_env():
