@@ -219,3 +219,48 @@ def test_device_tensor_out_and_determinism():
     # a slab does not depend on its neighbours in the batch
     solo = gm.forward_batch(exs[3:4])
     np.testing.assert_array_equal(solo[0], again[3])
+
+
+@pytest.mark.parametrize("binary", [False, True])
+def test_boxes_wider_than_32_voxels(binary, rng):
+    """res 0.1 A: an atom's box spans ~60 voxels per axis, exercising the
+    forward's >32-column path and the backward's sub-box walk."""
+    from conftest import random_coordinate_set
+    from paper_1912_04822_b200 import Example
+
+    exs = [Example(coord_sets=[random_coordinate_set(rng, 3, 2, 1.5)]) for _ in range(2)]
+    gm = gm_of({"resolution": 0.1, "dimension": 7.9, "binary": binary})  # D = 80
+    go = oracle.GridOracle(resolution=0.1, dimension=7.9, binary=binary)
+    grid, xf = gm.forward_batch(exs, random_rotation=True, rng=np.random.default_rng(4),
+                                return_transforms=True)
+    ref = go.forward_batch(exs, random_rotation=True, rng=np.random.default_rng(4))
+    if binary:
+        np.testing.assert_array_equal(grid, ref)
+        return
+    assert_close(grid, ref, what="wide-box forward")
+    gg = np.random.default_rng(5).standard_normal(grid.shape, dtype=np.float32)
+    got = gm.backward_batch(exs, gg, transforms=xf)
+    cgs, _ = go.backward_batch(exs, gg, random_rotation=True, rng=np.random.default_rng(4))
+    assert_close(np.concatenate([c for ex in got for (c, t) in ex]), np.concatenate(cgs),
+                 what="wide-box backward")
+
+
+def test_vector_many_channels_per_set(rng):
+    """> 16 channels in a set takes the per-channel vector backward path."""
+    from paper_1912_04822_b200 import CoordinateSet, Example
+
+    n, T = 12, 20
+    cs = CoordinateSet(coords=rng.uniform(-3, 3, (n, 3)).astype(np.float32),
+                       radii=rng.uniform(1.2, 2.0, n).astype(np.float32), num_types=T,
+                       type_vector=(rng.random((n, T)) * (rng.random((n, T)) < 0.3))
+                       .astype(np.float32))
+    exs = [Example(coord_sets=[cs])]
+    gm = gm_of({"dimension": 12.0})
+    go = oracle.GridOracle(dimension=12.0)
+    grid = gm.forward_batch(exs)
+    assert_close(grid, go.forward_batch(exs), what="forward")
+    gg = np.random.default_rng(2).standard_normal(grid.shape, dtype=np.float32)
+    (cg, tg), = gm.backward_batch(exs, gg)[0]
+    wc, wt = go.backward_batch(exs, gg)
+    assert_close(cg, wc[0], what="coord")
+    assert_close(tg, wt[0], what="type")
