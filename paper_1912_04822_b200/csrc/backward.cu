@@ -140,9 +140,10 @@ constexpr int kRows = 96;     // rows per chunk
 constexpr int kTab = 32;      // table entries per axis (sub-box edge)
 constexpr int kU = 4;         // 32-voxel windows per step (loads in flight per lane)
 
-struct __align__(16) RowEntry {
-    int start;   // offset of the row's first voxel in the flattened list
-    int kpack;   // k0 (relative to the sub-box) | (i_rel << 8) | (j_rel << 16)
+struct __align__(8) RowEntry {
+    int voff;    // grid offset of the row's voxel k minus its flattened index:
+                 // voxel v of the row sits at gbase + voff + v
+    int kz;      // table index of voxel v: kz + v
     double b2;   // dx^2 + dy^2
     double exy;  // Ex * Ey
     double dx, dy;
@@ -151,6 +152,7 @@ struct __align__(16) RowEntry {
 struct WarpBwd {
     double dz[kTab], ez[kTab], dx[kTab], ex[kTab], dy[kTab], ey[kTab];
     RowEntry rows[kRows];
+    unsigned starts[kRows * kTab / 32 + kU];  // bit v: a row starts at flattened voxel v
 };
 
 // f(slot, d2, R, dz, ez, voxel_offset, g): every voxel of the box with
@@ -186,6 +188,9 @@ __device__ __forceinline__ void flat_walk(const Atom &A, WarpBwd &W, const float
                 for (int rb = 0; rb < nrows_all; rb += kRows) {
                     // ---- phase 1: row spans, compacted with a warp scan ----
                     int nrow = 0, total = 0;
+                    const int nwords = (min(nrows_all - rb, kRows) * nk + 31) >> 5;
+                    for (int w = lane; w < nwords + kU; w += 32) W.starts[w] = 0u;
+                    __syncwarp();
                     const int rend = min(nrows_all, rb + kRows);
                     for (int r0 = rb; r0 < rend; r0 += 32) {
                         const int row = r0 + lane;
@@ -216,8 +221,10 @@ __device__ __forceinline__ void flat_walk(const Atom &A, WarpBwd &W, const float
                         const unsigned m = __ballot_sync(0xffffffffu, len > 0);
                         if (len > 0) {
                             RowEntry &R = W.rows[nrow + __popc(m & lt)];
-                            R.start = total + sc - len;
-                            R.kpack = klo | (ii << 8) | (jj << 16);
+                            const int st = total + sc - len;
+                            atomicOr(&W.starts[st >> 5], 1u << (st & 31));
+                            R.voff = (int)sbase + (ii * D + jj) * D + klo - st;
+                            R.kz = klo - st;
                             R.b2 = b2;
                             R.exy = W.ex[ii] * W.ey[jj];
                             R.dx = dx;
@@ -228,27 +235,20 @@ __device__ __forceinline__ void flat_walk(const Atom &A, WarpBwd &W, const float
                     }
                     __syncwarp();
                     // ---- phase 2: kU windows of 32 voxels per step ----
-                    int cur = 0;  // row containing the next window's first voxel
+                    // voxel v's row = (row starts <= v) - 1: one bitmap word per window
+                    const unsigned le = 0xffffffffu >> (31 - lane);
+                    int cur = -1;  // rows started before the next window, minus one
                     for (int base = 0; base < total; base += 32 * kU) {
                         int myrow[kU];
 #pragma unroll
                         for (int u = 0; u < kU; u++) {
-                            const int wb = base + 32 * u;
-                            unsigned bits = 0u;  // rows starting at window offsets 1..31
-                            bool at32 = false;
-                            const int q = cur + 1 + lane;
-                            if (q < nrow) {
-                                const int off = W.rows[q].start - wb;
-                                if (off > 0 && off < 32) bits = 1u << off;
-                                at32 = off == 32;
-                            }
-                            const unsigned M = __reduce_or_sync(0xffffffffu, bits);
-                            myrow[u] = cur + __popc(M & ((lt << 1) | 1u));
-                            cur += __popc(M) + (__any_sync(0xffffffffu, at32) ? 1 : 0);
+                            const unsigned M = W.starts[(base >> 5) + u];
+                            myrow[u] = cur + __popc(M & le);
+                            cur += __popc(M);
                         }
                         float g[kU];
                         int kk[kU];
-                        size_t vo[kU];
+                        int vo[kU];
 #pragma unroll
                         for (int u = 0; u < kU; u++) {
                             const int v = base + 32 * u + lane;
@@ -256,10 +256,9 @@ __device__ __forceinline__ void flat_walk(const Atom &A, WarpBwd &W, const float
                             kk[u] = 0;
                             vo[u] = 0;
                             if (v < total) {
-                                const int kp = W.rows[myrow[u]].kpack;
-                                kk[u] = (kp & 0xff) + (v - W.rows[myrow[u]].start);
-                                const int ii = (kp >> 8) & 0xff, jj = kp >> 16;
-                                vo[u] = sbase + ((size_t)ii * D + jj) * D + kk[u];
+                                const RowEntry &R = W.rows[myrow[u]];
+                                kk[u] = R.kz + v;
+                                vo[u] = R.voff + v;
                                 if (LOADG) g[u] = __ldg(gbase + vo[u]);
                             }
                         }
@@ -270,7 +269,7 @@ __device__ __forceinline__ void flat_walk(const Atom &A, WarpBwd &W, const float
                                 const RowEntry &R = W.rows[myrow[u]];
                                 const double dz = W.dz[kk[u]];
                                 const double d2 = fma(dz, dz, R.b2);
-                                f(u & 1, d2, R, dz, W.ez[kk[u]], vo[u], g[u]);
+                                f(u & 1, d2, R, dz, W.ez[kk[u]], (size_t)vo[u], g[u]);
                             }
                         }
                     }

@@ -7,7 +7,7 @@
 // Work decomposition (B200): one CTA per (example, channel, tile of TI planes
 // x TJ rows x all D columns); the tile accumulates in shared memory (dense
 // [TI][TJ][D]).  Each warp owns a disjoint region of the tile (one plane, or a
-// band of rows of one plane) and walks the channel's items (k_bin grouped them
+// band of rows of one plane) and walks the channel's items (k_prepare_example grouped them
 // by channel, in item order) 32 at a time:
 //   phase A (lane t <-> item t): box test against the region, the sphere's
 //           cross-section with the plane (row / column spans, ~2/3 of the box

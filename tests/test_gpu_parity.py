@@ -264,3 +264,24 @@ def test_vector_many_channels_per_set(rng):
     wc, wt = go.backward_batch(exs, gg)
     assert_close(cg, wc[0], what="coord")
     assert_close(tg, wt[0], what="type")
+
+
+@pytest.mark.parametrize("binary", [False, True])
+def test_example_too_big_for_smem_staging(binary, rng):
+    """6000 (atom, channel) items in one example: the prepare kernel stages
+    the records in the workspace instead of shared memory."""
+    from paper_1912_04822_b200 import CoordinateSet, Example
+
+    n, T = 600, 10
+    cs = CoordinateSet(coords=rng.uniform(-8, 8, (n, 3)).astype(np.float32),
+                       radii=rng.uniform(1.2, 2.0, n).astype(np.float32), num_types=T,
+                       type_vector=rng.uniform(0.1, 1.0, (n, T)).astype(np.float32))
+    exs = [Example(coord_sets=[cs]), Example(coord_sets=[cs])]
+    gm = gm_of({"dimension": 16.0, "binary": binary})
+    go = oracle.GridOracle(dimension=16.0, binary=binary)
+    grid = gm.forward_batch(exs, random_rotation=True, rng=np.random.default_rng(1))
+    ref = go.forward_batch(exs, random_rotation=True, rng=np.random.default_rng(1))
+    if binary:
+        np.testing.assert_array_equal(grid, ref)
+    else:
+        assert_close(grid, ref, what="global-staged forward")
