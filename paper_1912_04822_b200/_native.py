@@ -15,7 +15,8 @@ from pathlib import Path
 from .errors import DeviceError
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libgridmaker_b200.so"
+# GM_LIB: load a differently-tuned build of the same library (tools/variants.sh)
+LIB_PATH = Path(os.environ.get("GM_LIB") or PKG / "libgridmaker_b200.so")
 
 _c_int32 = ctypes.c_int32
 _c_int64 = ctypes.c_int64

@@ -33,7 +33,6 @@ struct BwdArgs {
     float *type_grad;
     const FwdItem *items;  // index mode: item a == atom a; its box (cut rmult*r) is reused
     double eg;             // exp(-2 grm^2), a batch constant (_kernels.py:224)
-    int dbg;
 };
 
 
@@ -135,17 +134,32 @@ __device__ __forceinline__ void store_coord(const BwdArgs &P, int a, int lane, d
 // starts inside its window (REDUX + popc).  Geometry and accumulation in
 // f64; the tail's 1/d from MUFU.RSQ64H + one Newton step.
 // ---------------------------------------------------------------------------
-constexpr int kBwdWarps = 4;
-constexpr int kRows = 96;     // rows per chunk
+#ifndef GM_BWD_WARPS
+#define GM_BWD_WARPS 1
+#endif
+constexpr int kBwdWarps = GM_BWD_WARPS;
+#ifndef GM_BWD_ROWS
+#define GM_BWD_ROWS 64
+#endif
+#ifndef GM_BWD_KU
+#define GM_BWD_KU 4
+#endif
+#ifndef GM_BWD_CHAINS
+#define GM_BWD_CHAINS 1
+#endif
+#ifndef GM_BWD_MINB
+#define GM_BWD_MINB 32
+#endif
+constexpr int kRows = GM_BWD_ROWS;  // rows per chunk
 constexpr int kTab = 32;      // table entries per axis (sub-box edge)
-constexpr int kU = 4;         // 32-voxel windows per step (loads in flight per lane)
+constexpr int kU = GM_BWD_KU;  // 32-voxel windows per step (loads in flight per lane)
 
 struct __align__(8) RowEntry {
     int voff;    // grid offset of the row's voxel k minus its flattened index:
                  // voxel v of the row sits at gbase + voff + v
     int kz;      // table index of voxel v: kz + v
     double b2;   // dx^2 + dy^2
-    double exy;  // Ex * Ey
+    double exy;  // Ex * Ey * exy_scale
     double dx, dy;
 };
 
@@ -159,7 +173,8 @@ struct WarpBwd {
 // d2 < dzr2 (others get g = 0 / are skipped), g loaded by the walk when LOADG.
 template <bool LOADG, typename F>
 __device__ __forceinline__ void flat_walk(const Atom &A, WarpBwd &W, const float *gbase, int D,
-                                          double res, float inv_res, int lane, F &&f) {
+                                          double res, float inv_res, int lane, double exy_scale,
+                                          F &&f) {
     const unsigned lt = (1u << lane) - 1u;
     const double dzr = A.dzr, dzr2 = A.dzr2;
     for (int si = A.i0; si <= A.i1; si += kTab)
@@ -226,7 +241,7 @@ __device__ __forceinline__ void flat_walk(const Atom &A, WarpBwd &W, const float
                             R.voff = (int)sbase + (ii * D + jj) * D + klo - st;
                             R.kz = klo - st;
                             R.b2 = b2;
-                            R.exy = W.ex[ii] * W.ey[jj];
+                            R.exy = (W.ex[ii] * W.ey[jj]) * exy_scale;
                             R.dx = dx;
                             R.dy = dy;
                         }
@@ -269,7 +284,7 @@ __device__ __forceinline__ void flat_walk(const Atom &A, WarpBwd &W, const float
                                 const RowEntry &R = W.rows[myrow[u]];
                                 const double dz = W.dz[kk[u]];
                                 const double d2 = fma(dz, dz, R.b2);
-                                f(u & 1, d2, R, dz, W.ez[kk[u]], (size_t)vo[u], g[u]);
+                                f(GM_BWD_CHAINS > 1 ? (u & 1) : 0, d2, R, dz, W.ez[kk[u]], (size_t)vo[u], g[u]);
                             }
                         }
                     }
@@ -278,7 +293,7 @@ __device__ __forceinline__ void flat_walk(const Atom &A, WarpBwd &W, const float
             }
 }
 
-__global__ void __launch_bounds__(kBwdWarps * 32, 6) k_backward_index(const BwdArgs P) {
+__global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(const BwdArgs P) {
     __shared__ WarpBwd wsm[kBwdWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int a = blockIdx.x * kBwdWarps + warp;
@@ -311,7 +326,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 6) k_backward_index(const BwdA
     if (A.i0 <= A.i1 && A.j0 <= A.j1 && A.k0 <= A.k1) {
         const float *gbase = P.grid_grad + ((size_t)e * b.nchannels + c) * ((size_t)D * D * D);
         const double dzr = A.dzr, dzr2 = A.dzr2;
-        flat_walk<true>(A, wsm[warp], gbase, D, res, inv_res, lane,
+        const double qa2dzr = qa2 * dzr;
+        flat_walk<true>(A, wsm[warp], gbase, D, res, inv_res, lane, m4inv_r2,
                         [&](int slot, double d2, const RowEntry &R, double dz, double ez, size_t,
                             float g) {
                             // slope/d: Gaussian exp(-2d^2/r^2)(-4/r^2) (separable factors);
@@ -319,9 +335,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 6) k_backward_index(const BwdA
                             const bool in = d2 > 0.0 && d2 < dzr2;
                             const double gv = in ? widen(g) : 0.0;
                             const double rd = rsqrt_d(d2);
-                            const double sq = gv * qa2 * fma(-dzr, rd, 1.0);
-                            const double sg = gv * (R.exy * ez) * m4inv_r2;
-                            const double scl = d2 <= d02 ? sg : sq;
+                            // R.exy carries -4/r^2: Gaussian factor Ex Ey Ez (-4/r^2)
+                            const double t = d2 <= d02 ? R.exy * ez : fma(-qa2dzr, rd, qa2);
+                            const double scl = gv * t;
                             if (slot) {
                                 g1x = fma(scl, R.dx, g1x);
                                 g1y = fma(scl, R.dy, g1y);
@@ -373,7 +389,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_backward_vector(const BwdArg
         }
         if (set_radius(A, r, rmult, res, D)) {
             const double dzr = A.dzr, dzr2 = A.dzr2;
-            flat_walk<false>(A, wsm[warp], gset, D, res, inv_res, lane,
+            flat_walk<false>(A, wsm[warp], gset, D, res, inv_res, lane, 1.0,
                              [&](int, double d2, const RowEntry &R, double dz, double ez,
                                  size_t voff, float) {
                                  if (d2 >= dzr2) return;
@@ -428,7 +444,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_backward_vector(const BwdArg
             double tg = 0.0;
             if (set_radius(A, r, rmult, res, D)) {
                 const double dzr = A.dzr, dzr2 = A.dzr2;
-                flat_walk<true>(A, wsm[warp], gset + (size_t)c * D3, D, res, inv_res, lane,
+                flat_walk<true>(A, wsm[warp], gset + (size_t)c * D3, D, res, inv_res, lane, 1.0,
                                 [&](int, double d2, const RowEntry &R, double dz, double ez,
                                     size_t, float gf) {
                                     if (d2 >= dzr2 || gf == 0.0f) return;
@@ -473,10 +489,6 @@ gm_status backward_impl(const gm_params *p, const gm_batch *b, const Workspace &
     P.type_grad = type_grad;
     P.items = ws.items;
     P.eg = exp((-2.0 * p->gaussian_radius_multiple) * p->gaussian_radius_multiple);
-    {
-        const char *d = getenv("GM_DEBUG_BWD");
-        P.dbg = d ? atoi(d) : 0;
-    }
     if (b->vector_mode)
         k_backward_vector<<<(b->natoms + kBwdWarps - 1) / kBwdWarps, kBwdWarps * 32, 0, s>>>(P);
     else

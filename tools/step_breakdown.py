@@ -50,3 +50,5 @@ timeit("forward_packed+backward_packed", lambda: (
 timeit("step with draw", lambda: (
     gm.forward_packed(pb, out, transforms=geom.draw_transform_array(pb.default_centers, 2.0, True, rng)),
     gm.backward_packed(pb, gg, reuse_prepared=True, coord_grad=cg)))
+timeit("torch zero_ of the output (write roofline)", lambda: out.zero_())
+timeit("torch copy out <- gg (read+write)", lambda: out.copy_(gg))
