@@ -74,6 +74,8 @@ struct Workspace {
     BinItem *bsorted;    // nitems (binary mode)
     int2 *sbox;          // nitems: {ibox, jbox} of sorted items (forward culling)
     int32_t *chan_off;   // nexamples * (nchannels + 1): ranges into sorted
+    int4 *chan_job;      // nexamples * nchannels, channels by item count, descending:
+                         // {channel, first item, end item, 0} (the forward's job table)
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -98,6 +100,7 @@ inline size_t carve_workspace(void *base, int32_t natoms, int32_t nitems, int32_
     ws->bsorted = (BinItem *)take(sizeof(BinItem) * ni);
     ws->sbox = (int2 *)take(sizeof(int2) * ni);
     ws->chan_off = (int32_t *)take(sizeof(int32_t) * (size_t)std::max(nex, 1) * (nch + 1));
+    ws->chan_job = (int4 *)take(sizeof(int4) * (size_t)std::max(nex, 1) * std::max(nch, 1));
     return off + 256;
 }
 

@@ -18,19 +18,37 @@
 // Regions are disjoint and each warp adds its items in order, so every voxel
 // is summed in the reference's item order without atomics.  The finished tile
 // (zeros included) leaves through TMA bulk stores (cp.async.bulk) when
-// D % 4 == 0: the planes of a tile are contiguous in global memory.  CTAs
-// whose channel has no item only stream zeros.
+// D % 4 == 0: the planes of a tile are contiguous in global memory.
+// Consecutive CTAs are the channels of one tile, so scatter work and the
+// stores of empty channels interleave finely (HBM keeps writing while SMs
+// compute).
 #include "common.cuh"
 
 namespace {
 
-constexpr int kThreads = 128;
+#ifndef GM_FWD_WARPS
+#define GM_FWD_WARPS 4
+#endif
+#ifndef GM_FWD_MINB
+#define GM_FWD_MINB 5
+#endif
+#ifndef GM_FWD_ORDER
+#define GM_FWD_ORDER 0  // 1: channels of a tile heaviest first (job table)
+#endif
+#ifndef GM_FWD_ZERO_BULK
+#define GM_FWD_ZERO_BULK 1  // zero channels leave through the bulk-store path
+#endif
+#ifndef GM_FWD_BUDGET_KB
+#define GM_FWD_BUDGET_KB 37
+#endif
+constexpr int kThreads = 32 * GM_FWD_WARPS;
 constexpr int kWarps = kThreads / 32;
 
 struct FwdArgs {
     const FwdItem *sorted;
     const BinItem *bsorted;
     const int2 *sbox;
+    const int4 *chan_job;
     const int32_t *chan_off;
     const double *origins;
     float *out;
@@ -129,20 +147,36 @@ __device__ __forceinline__ bool plan_visit(const FwdItem &it, int i, int jg0, in
 }
 
 template <bool BINARY, bool VECTOR, bool RESL>
-__global__ void __launch_bounds__(kThreads, 5) k_forward(const FwdArgs A) {
+__global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs A) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int c = blockIdx.x % A.C, tile = blockIdx.x / A.C, e = blockIdx.y;
+    // grid (rank, tile, example): rank r of example e is its r-th heaviest
+    // channel (job table: channel and item range).  Consecutive CTAs are the
+    // channels of one tile, heavy ones first: scatter work and zero-tile
+    // stores interleave finely, which keeps HBM writing while SMs compute.
+    const int tile = blockIdx.y, e = blockIdx.z, rank = blockIdx.x;
+    int c, cs, ce;
+    if (GM_FWD_ORDER) {
+        const int4 J = A.chan_job[(size_t)e * A.C + rank];
+        c = J.x;
+        cs = J.y;
+        ce = J.z;
+    } else {
+        c = rank;
+        cs = A.chan_off[(size_t)e * (A.C + 1) + c];
+        ce = A.chan_off[(size_t)e * (A.C + 1) + c + 1];
+    }
     const int D = A.D, TI = A.TI, TJ = A.TJ;
     const int i0 = (tile / A.ntj) * TI, j0 = (tile % A.ntj) * TJ;
     const int TIv = min(TI, D - i0), TJv = min(TJ, D - j0);
     const size_t plane = (size_t)D * D;
     float *obase = A.out + ((size_t)e * A.C + c) * D * plane + (size_t)i0 * plane + (size_t)j0 * D;
     const int chunk = TJv * D;  // contiguous floats per plane of the tile (global and smem)
-    const int32_t *co = A.chan_off + (size_t)e * (A.C + 1) + c;
-    const int cs = co[0], ce = co[1];
 
-    if (cs == ce) {  // no item of this channel: stream zeros
+    // no item of this channel and no bulk path: stream zeros (with the bulk
+    // path the zeroed accumulator leaves through one bulk store, which frees
+    // the CTA sooner than a loop of stores)
+    if (cs == ce && !(GM_FWD_ZERO_BULK && A.bulk)) {
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
         if (A.bulk && TJv == D) {
             // the tile's planes are one contiguous run
@@ -333,7 +367,7 @@ struct FwdConfig {
 };
 
 FwdConfig choose_config(int D) {
-    const size_t budget = 37 * 1024;  // acc; + 8 KB of slots -> 5 CTAs per SM
+    const size_t budget = GM_FWD_BUDGET_KB * 1024;  // acc; + 2 KB of slots per warp
     const size_t plane = (size_t)D * D * 4;
     FwdConfig cfg{};
     int TI = kWarps;
@@ -354,7 +388,8 @@ gm_status launch(const FwdArgs &A, const FwdConfig &cfg, int nex, cudaStream_t s
     auto kern = k_forward<BIN, VEC, RESL>;
     CUDA_TRY(gm_ensure_smem((const void *)kern, (int)cfg.smem));
     const int ntiles = ((A.D + cfg.TI - 1) / cfg.TI) * A.ntj;
-    dim3 grid(ntiles * A.C, nex);
+    if (ntiles > 65535 || nex > 65535) return gm_fail(GM_ERR_INVALID, "too many examples or tiles");
+    dim3 grid(A.C, ntiles, nex);
     kern<<<grid, kThreads, cfg.smem, s>>>(A);
     LAUNCH_CHECK();
     return GM_OK;
@@ -371,6 +406,7 @@ gm_status forward_impl(const gm_params *p, const gm_batch *b, const Workspace &w
     A.sorted = ws.sorted;
     A.bsorted = ws.bsorted;
     A.sbox = ws.sbox;
+    A.chan_job = ws.chan_job;
     A.chan_off = ws.chan_off;
     A.origins = b->origins;
     A.out = out;

@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(1024) k_prepare_example(const PrepArgs A) {
     int *rank = chs + n;
     int *tab = rank + n;  // [nchunk][C]
     int *off = tab + nchunk * C;
+    int *crank = off + C + 1;  // [C]
     for (int t = threadIdx.x; t < nchunk * C; t += blockDim.x) tab[t] = 0;
     if (vector) {  // positions of all atoms (items only see atoms that have weights)
         for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < b.natoms;
@@ -208,16 +209,42 @@ __global__ void __launch_bounds__(1024) k_prepare_example(const PrepArgs A) {
         off[c] = s;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int pos = is;
+    if (warp == 0) {
+        // The forward's job table: channels by item count, descending (ties by
+        // channel), so it schedules the heaviest tiles first and ends on the
+        // cheap ones; each entry carries the channel's item range.
+        int4 *jobs = A.ws.chan_job + (size_t)e * C;
         int32_t *co = A.ws.chan_off + (size_t)e * (C + 1);
-        for (int c = 0; c < C; c++) {
+        for (int c = lane; c < C; c += 32) {
             const int k = off[c];
-            off[c] = pos;
-            co[c] = pos;
-            pos += k;
+            int rk = 0;
+            for (int q = 0; q < C; q++) {
+                const int kq = off[q];
+                rk += (kq > k) || (kq == k && q < c);
+            }
+            crank[c] = rk;
         }
-        co[C] = pos;
+        __syncwarp();
+        int pos = is;
+        for (int c0 = 0; c0 < C; c0 += 32) {
+            const int c = c0 + lane;
+            const int k = c < C ? off[c] : 0;
+            int sc = k;  // inclusive scan of the counts
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, sc, o);
+                if (lane >= o) sc += t;
+            }
+            __syncwarp();
+            if (c < C) {
+                const int st = pos + sc - k;
+                off[c] = st;
+                co[c] = st;
+                jobs[crank[c]] = make_int4(c, st, st + k, 0);
+            }
+            pos += __shfl_sync(0xffffffffu, sc, 31);
+        }
+        if (lane == 0) co[C] = pos;
     }
     __syncthreads();
     // 16-byte chunks, coalesced within a record
@@ -252,7 +279,7 @@ gm_status prepare_impl(const gm_params *p, const gm_batch *b, const Workspace &w
     }
     if (b->max_example_items < 0) return gm_fail(GM_ERR_INVALID, "max_example_items < 0");
     const size_t n = (size_t)b->max_example_items, nchunk = (n + 31) / 32;
-    const size_t base = sizeof(int) * (2 * n + nchunk * b->nchannels + b->nchannels + 1);
+    const size_t base = sizeof(int) * (2 * n + nchunk * b->nchannels + 2 * b->nchannels + 1);
     const size_t staged = base + n * (sizeof(FwdItem) + (p->binary ? sizeof(BinItem) : 0));
     const size_t limit = 200 * 1024;
     if (base > limit)

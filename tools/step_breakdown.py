@@ -52,3 +52,36 @@ timeit("step with draw", lambda: (
     gm.backward_packed(pb, gg, reuse_prepared=True, coord_grad=cg)))
 timeit("torch zero_ of the output (write roofline)", lambda: out.zero_())
 timeit("torch copy out <- gg (read+write)", lambda: out.copy_(gg))
+
+# forward of one batch overlapped with the backward of another (two streams)
+pb2 = gm.pack(exs)
+p2 = gm._prepare(pb2, None, xf, D)
+out2 = torch.empty_like(out)
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+torch.cuda.synchronize()
+
+
+def overlapped():
+    with torch.cuda.stream(s1):
+        lib.gm_forward(ctypes.byref(p), ctypes.byref(pb._gm), ws, out.data_ptr(), s1.cuda_stream)
+    with torch.cuda.stream(s2):
+        lib.gm_backward(ctypes.byref(p2), ctypes.byref(pb2._gm), pb2.workspace.data_ptr(),
+                        gg.data_ptr(), cg.data_ptr(), None, s2.cuda_stream)
+
+
+for _ in range(5):
+    overlapped()
+torch.cuda.synchronize()
+import time
+t = time.perf_counter()
+for _ in range(200):
+    overlapped()
+torch.cuda.synchronize()
+print(f"{'fwd || bwd on two streams':40s} {(time.perf_counter() - t) / 200 * 1e6:8.1f} us (wall)")
+t = time.perf_counter()
+for _ in range(200):
+    lib.gm_forward(ctypes.byref(p), ctypes.byref(pb._gm), ws, out.data_ptr(), st)
+    lib.gm_backward(ctypes.byref(p2), ctypes.byref(pb2._gm), pb2.workspace.data_ptr(),
+                    gg.data_ptr(), cg.data_ptr(), None, st)
+torch.cuda.synchronize()
+print(f"{'fwd ; bwd on one stream':40s} {(time.perf_counter() - t) / 200 * 1e6:8.1f} us (wall)")
