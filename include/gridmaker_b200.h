@@ -87,6 +87,13 @@ typedef struct {
     /* per example */
     const double *origins;           /* (nexamples,3) center - dimension/2 */
     const double *xforms;            /* (nexamples,15) R row-major, center, translation; NULL = none */
+    /* optional static grouping, computed once when the batch is packed (or NULL):
+     * item_perm (nitems) lists example e's items in (channel, item) order in
+     * slots [ex_item_start[e], ex_item_end[e]); chan_off (nexamples, nchannels+1)
+     * holds each channel's absolute slot range.  With both, gm_prepare_inline is
+     * one fully parallel pass. */
+    const int32_t *item_perm;
+    const int32_t *chan_off;
 } gm_batch;
 
 /* Device scratch needed by gm_prepare / gm_forward / gm_backward. */
@@ -94,6 +101,17 @@ size_t gm_workspace_bytes(int32_t natoms, int32_t nitems, int32_t nexamples, int
 
 gm_status gm_prepare(const gm_params *p, const gm_batch *b, void *workspace,
                      size_t workspace_bytes, void *stream);
+/* gm_prepare with the per-call arrays in HOST memory: origins_host (nexamples,3)
+ * and xforms_host (nexamples,15) or NULL.  With a static grouping (item_perm,
+ * chan_off) and nexamples <= GM_INLINE_MAX_EXAMPLES they travel inside the
+ * kernel launch (no separate copy; the host arrays may be reused as soon as the
+ * call returns); otherwise they are copied to b->origins / b->xforms first.
+ * b->origins must be a device buffer of (nexamples,3) either way: the prepare
+ * pass stores the origins there for gm_forward / gm_backward. */
+#define GM_INLINE_MAX_EXAMPLES 200
+gm_status gm_prepare_inline(const gm_params *p, const gm_batch *b, void *workspace,
+                            size_t workspace_bytes, const double *origins_host,
+                            const double *xforms_host, void *stream);
 /* out: (nexamples, nchannels, D, D, D) f32 device; every voxel is written. */
 gm_status gm_forward(const gm_params *p, const gm_batch *b, const void *workspace,
                      float *out, void *stream);

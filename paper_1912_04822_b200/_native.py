@@ -56,13 +56,15 @@ class GmBatch(ctypes.Structure):
         ("item_atom", _vp), ("item_channel", _vp), ("item_weight", _vp), ("item_radius", _vp),
         ("ex_item_start", _vp), ("ex_item_end", _vp), ("max_example_items", _c_int32),
         ("origins", _vp), ("xforms", _vp),
+        ("item_perm", _vp), ("chan_off", _vp),
     ]
 
 
 _LIB = None
+INLINE_MAX_EXAMPLES = 200  # GM_INLINE_MAX_EXAMPLES
 
 EXPORTS = (
-    "gm_workspace_bytes", "gm_prepare", "gm_forward", "gm_backward", "gm_workspace_positions",
+    "gm_workspace_bytes", "gm_prepare", "gm_prepare_inline", "gm_forward", "gm_backward", "gm_workspace_positions",
     "gm_forward_index_sets_host", "gm_forward_vector_sets_host", "gm_backward_index_host",
     "gm_backward_vector_host", "gm_last_error", "gm_version", "gm_device_count",
     "gm_launch_count", "gm_struct_size", "gm_draw_transforms",
@@ -85,6 +87,8 @@ def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     L.gm_workspace_bytes.restype = _c_size_t
     L.gm_prepare.argtypes = [P(GmParams), P(GmBatch), _vp, _c_size_t, _vp]
     L.gm_prepare.restype = ctypes.c_int
+    L.gm_prepare_inline.argtypes = [P(GmParams), P(GmBatch), _vp, _c_size_t, _vp, _vp, _vp]
+    L.gm_prepare_inline.restype = ctypes.c_int
     L.gm_forward.argtypes = [P(GmParams), P(GmBatch), _vp, _vp, _vp]
     L.gm_forward.restype = ctypes.c_int
     L.gm_backward.argtypes = [P(GmParams), P(GmBatch), _vp, _vp, _vp, _vp, _vp]

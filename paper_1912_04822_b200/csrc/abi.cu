@@ -9,7 +9,7 @@
 
 #include "common.cuh"
 
-#define GM_VERSION "gridmaker_b200 0.2.0 (sm_100a)"
+#define GM_VERSION "gridmaker_b200 0.3.0 (sm_100a)"
 
 static thread_local std::string g_err;
 static std::atomic<int64_t> g_launches{0};
@@ -93,6 +93,39 @@ extern "C" gm_status gm_prepare(const gm_params *p, const gm_batch *b, void *wor
     if (b->nitems > 0 && !b->item_channel && !b->atom_type)
         return gm_fail(GM_ERR_INVALID, "items need item_channel or atom_type");
     return prepare_impl(p, b, ws_of(workspace, b), (cudaStream_t)stream, true);
+}
+
+extern "C" gm_status gm_prepare_inline(const gm_params *p, const gm_batch *b, void *workspace,
+                                       size_t workspace_bytes, const double *origins_host,
+                                       const double *xforms_host, void *stream) {
+    gm_status st = check_params(p);
+    if (st) return st;
+    if ((st = check_batch(b))) return st;
+    if (!origins_host && b->nexamples > 0) return gm_fail(GM_ERR_INVALID, "origins_host is NULL");
+    if (!b->origins && b->nexamples > 0) return gm_fail(GM_ERR_INVALID, "b->origins is NULL");
+    const size_t need = gm_workspace_bytes(b->natoms, b->nitems, b->nexamples, b->nchannels);
+    if (!workspace || workspace_bytes < need)
+        return gm_fail(GM_ERR_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, need);
+    if (!b->vector_mode && b->nitems != b->natoms)
+        return gm_fail(GM_ERR_INVALID, "index mode needs one item per atom");
+    if (b->nitems > 0 && !b->item_channel && !b->atom_type)
+        return gm_fail(GM_ERR_INVALID, "items need item_channel or atom_type");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (b->item_perm && b->chan_off && b->nexamples <= GM_INLINE_MAX_EXAMPLES)
+        return prepare_inline_impl(p, b, ws_of(workspace, b), origins_host, xforms_host, s);
+    // general path: stage the per-call arrays, then the per-example grouping pass
+    if (xforms_host && !b->xforms) return gm_fail(GM_ERR_INVALID, "b->xforms is NULL");
+    if (b->nexamples > 0) {
+        CUDA_TRY(cudaMemcpyAsync(const_cast<double *>(b->origins), origins_host,
+                                 sizeof(double) * 3 * b->nexamples, cudaMemcpyHostToDevice, s));
+        if (xforms_host)
+            CUDA_TRY(cudaMemcpyAsync(const_cast<double *>(b->xforms), xforms_host,
+                                     sizeof(double) * 15 * b->nexamples, cudaMemcpyHostToDevice,
+                                     s));
+    }
+    gm_batch bb = *b;
+    if (!xforms_host) bb.xforms = nullptr;
+    return prepare_impl(p, &bb, ws_of(workspace, b), s, true);
 }
 
 extern "C" gm_status gm_forward(const gm_params *p, const gm_batch *b, const void *workspace,

@@ -74,8 +74,6 @@ struct Workspace {
     BinItem *bsorted;    // nitems (binary mode)
     int2 *sbox;          // nitems: {ibox, jbox} of sorted items (forward culling)
     int32_t *chan_off;   // nexamples * (nchannels + 1): ranges into sorted
-    int4 *chan_job;      // nexamples * nchannels, channels by item count, descending:
-                         // {channel, first item, end item, 0} (the forward's job table)
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -100,7 +98,6 @@ inline size_t carve_workspace(void *base, int32_t natoms, int32_t nitems, int32_
     ws->bsorted = (BinItem *)take(sizeof(BinItem) * ni);
     ws->sbox = (int2 *)take(sizeof(int2) * ni);
     ws->chan_off = (int32_t *)take(sizeof(int32_t) * (size_t)std::max(nex, 1) * (nch + 1));
-    ws->chan_job = (int4 *)take(sizeof(int4) * (size_t)std::max(nex, 1) * std::max(nch, 1));
     return off + 256;
 }
 
@@ -137,6 +134,8 @@ __device__ __forceinline__ int small_div(int a, float inv_b) {
 // ---------------------------------------------------------------------------
 gm_status prepare_impl(const gm_params *p, const gm_batch *b, const Workspace &ws,
                        cudaStream_t s, bool items_too);
+gm_status prepare_inline_impl(const gm_params *p, const gm_batch *b, const Workspace &ws,
+                              const double *origins, const double *xforms, cudaStream_t s);
 gm_status forward_impl(const gm_params *p, const gm_batch *b, const Workspace &ws, float *out,
                        cudaStream_t s);
 gm_status backward_impl(const gm_params *p, const gm_batch *b, const Workspace &ws,

@@ -6,9 +6,10 @@
 //
 // Work decomposition (B200): one CTA per (example, channel, tile of TI planes
 // x TJ rows x all D columns); the tile accumulates in shared memory (dense
-// [TI][TJ][D]).  Each warp owns a disjoint region of the tile (one plane, or a
-// band of rows of one plane) and walks the channel's items (k_prepare_example grouped them
-// by channel, in item order) 32 at a time:
+// [TI][TJ][D]).  Default: one-warp CTAs owning one plane (48^3: 9 KB, 16
+// CTAs per SM; 96^3: a band of rows) -- no warp waits for another.  Each warp
+// owns a disjoint region of the tile and walks the channel's items
+// (k_prepare_example grouped them by channel, in item order) 32 at a time:
 //   phase A (lane t <-> item t): box test against the region, the sphere's
 //           cross-section with the plane (row / column spans, ~2/3 of the box
 //           face), per-visit constants -> a per-warp shared-memory slot;
@@ -27,19 +28,16 @@
 namespace {
 
 #ifndef GM_FWD_WARPS
-#define GM_FWD_WARPS 4
+#define GM_FWD_WARPS 1
 #endif
 #ifndef GM_FWD_MINB
-#define GM_FWD_MINB 5
-#endif
-#ifndef GM_FWD_ORDER
-#define GM_FWD_ORDER 0  // 1: channels of a tile heaviest first (job table)
+#define GM_FWD_MINB 16
 #endif
 #ifndef GM_FWD_ZERO_BULK
 #define GM_FWD_ZERO_BULK 1  // zero channels leave through the bulk-store path
 #endif
 #ifndef GM_FWD_BUDGET_KB
-#define GM_FWD_BUDGET_KB 37
+#define GM_FWD_BUDGET_KB 10
 #endif
 constexpr int kThreads = 32 * GM_FWD_WARPS;
 constexpr int kWarps = kThreads / 32;
@@ -48,7 +46,6 @@ struct FwdArgs {
     const FwdItem *sorted;
     const BinItem *bsorted;
     const int2 *sbox;
-    const int4 *chan_job;
     const int32_t *chan_off;
     const double *origins;
     float *out;
@@ -150,22 +147,13 @@ template <bool BINARY, bool VECTOR, bool RESL>
 __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs A) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // grid (rank, tile, example): rank r of example e is its r-th heaviest
-    // channel (job table: channel and item range).  Consecutive CTAs are the
-    // channels of one tile, heavy ones first: scatter work and zero-tile
-    // stores interleave finely, which keeps HBM writing while SMs compute.
-    const int tile = blockIdx.y, e = blockIdx.z, rank = blockIdx.x;
-    int c, cs, ce;
-    if (GM_FWD_ORDER) {
-        const int4 J = A.chan_job[(size_t)e * A.C + rank];
-        c = J.x;
-        cs = J.y;
-        ce = J.z;
-    } else {
-        c = rank;
-        cs = A.chan_off[(size_t)e * (A.C + 1) + c];
-        ce = A.chan_off[(size_t)e * (A.C + 1) + c + 1];
-    }
+    // grid (channel, tile, example): consecutive CTAs are the channels of one
+    // tile, so scatter work and zero-tile stores interleave finely, which
+    // keeps HBM writing while SMs compute
+    const int tile = blockIdx.y, e = blockIdx.z, rank = blockIdx.x;  // rank = channel
+    const int c = rank;
+    const int cs = A.chan_off[(size_t)e * (A.C + 1) + c];
+    const int ce = A.chan_off[(size_t)e * (A.C + 1) + c + 1];
     const int D = A.D, TI = A.TI, TJ = A.TJ;
     const int i0 = (tile / A.ntj) * TI, j0 = (tile % A.ntj) * TJ;
     const int TIv = min(TI, D - i0), TJv = min(TJ, D - j0);
@@ -406,7 +394,6 @@ gm_status forward_impl(const gm_params *p, const gm_batch *b, const Workspace &w
     A.sorted = ws.sorted;
     A.bsorted = ws.bsorted;
     A.sbox = ws.sbox;
-    A.chan_job = ws.chan_job;
     A.chan_off = ws.chan_off;
     A.origins = b->origins;
     A.out = out;

@@ -5,7 +5,12 @@
 //                      hi/lo coordinates, density constants (_kernels.py:81-85);
 //                      stable grouping of the items by output channel, so each
 //                      forward CTA reads only its channel's items, in order
+//   k_prepare_static   batches packed with a static grouping (gm_batch.item_perm):
+//                      the same records in one fully parallel pass, per-call
+//                      arrays inside the launch
 //   k_prepare_atoms    positions only (backward without a forward)
+#include <string.h>
+
 #include "common.cuh"
 
 struct PrepArgs {
@@ -34,9 +39,11 @@ __device__ __forceinline__ double dot3(const double a[3], const double *b, int o
     }
 }
 
-// geom.py:105: x' = ((x - c) @ R.T + c) + t in float64.  Without a transform
+// geom.py:105: x' = ((x - c) @ R.T + c) + t in float64, X = the example's
+// transform (R row-major, center, translation) or NULL.  Without a transform
 // the float32 input is widened exactly (voxelizer.py:366).
-__device__ __forceinline__ void transform_atom(const PrepArgs &A, int a, double x[3]) {
+__device__ __forceinline__ void transform_atom_x(const PrepArgs &A, int a, int s, const double *X,
+                                                 double x[3]) {
     const gm_batch &b = A.b;
     if (b.coords64) {
         x[0] = b.coords64[3 * a + 0];
@@ -47,10 +54,7 @@ __device__ __forceinline__ void transform_atom(const PrepArgs &A, int a, double 
         x[1] = (double)b.coords32[3 * a + 1];
         x[2] = (double)b.coords32[3 * a + 2];
     }
-    if (b.xforms) {
-        const int s = b.atom_set[a];
-        const int e = b.set_example[s];
-        const double *X = b.xforms + 15 * (size_t)e;
+    if (X) {
         const int nset = b.set_end[s] - b.set_start[s];
         const int order = nset == 1 ? A.p.matmul_order_1 : A.p.matmul_order_n;
         const double d[3] = {__dsub_rn(x[0], X[9]), __dsub_rn(x[1], X[10]),
@@ -59,6 +63,13 @@ __device__ __forceinline__ void transform_atom(const PrepArgs &A, int a, double 
         for (int j = 0; j < 3; j++)
             x[j] = __dadd_rn(__dadd_rn(dot3(d, X + 3 * j, order), X[9 + j]), X[12 + j]);
     }
+}
+
+__device__ __forceinline__ void transform_atom(const PrepArgs &A, int a, double x[3]) {
+    const gm_batch &b = A.b;
+    const int s = b.atom_set[a];
+    const double *X = b.xforms ? b.xforms + 15 * (size_t)b.set_example[s] : nullptr;
+    transform_atom_x(A, a, s, X, x);
 }
 
 __device__ __forceinline__ void store_pos(const PrepArgs &A, int a, const double x[3]) {
@@ -86,19 +97,18 @@ __device__ __forceinline__ void split_hilo(double v, float &hi, float &lo) {
 // The forward record of item `it` (atom a at transformed position x):
 // _kernels.py:22-30 boxes, grid-local hi/lo corner offsets, density constants
 // (_kernels.py:81-85).  Returns its channel, or -1 when the box misses the grid.
-__device__ __forceinline__ int make_item(const PrepArgs &A, int it, int a, const double x3[3],
-                                         FwdItem &f, BinItem &bi) {
+__device__ __forceinline__ int make_item_o(const PrepArgs &A, int it, int a, int s,
+                                           const double *O, const double x3[3], FwdItem &f,
+                                           BinItem &bi) {
     const gm_batch &b = A.b;
     const gm_params &p = A.p;
     const int D = p.npts;
     const double res = p.resolution, grm = p.gaussian_radius_multiple, rmult = p.radius_multiple;
-    const int s = b.atom_set[a];
-    const int e = b.set_example[s];
     const int ch = b.set_choff[s] + (b.item_channel ? b.item_channel[it] : b.atom_type[a]);
     const double r = b.item_radius ? b.item_radius[it] : b.atom_radius[a];
     const float w = b.item_weight ? b.item_weight[it] : 1.0f;
     const double x = x3[0], y = x3[1], z = x3[2];
-    const double ox = b.origins[3 * e + 0], oy = b.origins[3 * e + 1], oz = b.origins[3 * e + 2];
+    const double ox = O[0], oy = O[1], oz = O[2];
     // _kernels.py:55/74 (index), 144/167 (vector): cut = r (binary) or r * rmult
     const double cut = p.binary ? r : __dmul_rn(r, rmult);
     int i0, i1, j0, j1, k0, k1;
@@ -125,6 +135,78 @@ __device__ __forceinline__ int make_item(const PrepArgs &A, int it, int a, const
     f.atom = a;
     bi = BinItem{x, y, z, __dmul_rn(r, r)};
     return valid ? ch : -1;
+}
+
+__device__ __forceinline__ int make_item(const PrepArgs &A, int it, int a, const double x3[3],
+                                         FwdItem &f, BinItem &bi) {
+    const int s = A.b.atom_set[a];
+    return make_item_o(A, it, a, s, A.b.origins + 3 * (size_t)A.b.set_example[s], x3, f, bi);
+}
+
+// ---------------------------------------------------------------------------
+// Static grouping (gm_batch.item_perm / chan_off, computed when the batch is
+// packed): one fully parallel pass, thread t <-> grouped slot t.  The per-call
+// arrays (origins, transforms) travel inside the launch (kernel parameters,
+// up to CAP examples): no separate host->device copy.  Items whose box misses
+// the grid stay in their channel's range with an empty box (ibox lo > hi), so
+// the forward's cull and the backward's box test skip them.
+// ---------------------------------------------------------------------------
+template <int CAP>
+struct CallArgs {
+    int nex, has_xf;
+    double v[18 * CAP];  // origins (nex,3), then transforms (nex,15)
+};
+
+template <int CAP>
+__global__ void __launch_bounds__(256) k_prepare_static(const PrepArgs A, const __grid_constant__ CallArgs<CAP> K) {
+    const gm_batch &b = A.b;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nex = K.nex;
+    const bool vector = b.item_atom != nullptr;
+    if (t < 3 * nex) const_cast<double *>(b.origins)[t] = K.v[t];  // for forward / backward
+    if (t < nex * (b.nchannels + 1)) A.ws.chan_off[t] = b.chan_off[t];
+    if (vector && t < b.natoms) {  // positions of all atoms
+        const int s = b.atom_set[t];
+        const int e = b.set_example[s];
+        double x[3];
+        transform_atom_x(A, t, s, K.has_xf ? K.v + 3 * nex + 15 * e : nullptr, x);
+        store_pos(A, t, x);
+    }
+    if (t < b.nitems) {
+        const int it = b.item_perm[t];
+        const int a = vector ? b.item_atom[it] : it;
+        const int s = b.atom_set[a];
+        const int e = b.set_example[s];
+        double x[3];
+        transform_atom_x(A, a, s, K.has_xf ? K.v + 3 * nex + 15 * e : nullptr, x);
+        if (!vector) store_pos(A, a, x);
+        FwdItem f;
+        BinItem bi;
+        if (make_item_o(A, it, a, s, K.v + 3 * e, x, f, bi) < 0) f.ibox = 0x7fff;  // empty
+        A.ws.sorted[t] = f;
+        A.ws.sbox[t] = make_int2(f.ibox, f.jbox);
+        if (A.p.binary) A.ws.bsorted[t] = bi;
+        // packed order: the index-mode backward reads its boxes
+        *reinterpret_cast<int4 *>(&A.ws.items[it].ibox) = make_int4(f.ibox, f.jbox, f.kbox, f.atom);
+    }
+}
+
+template <int CAP>
+gm_status launch_static(const PrepArgs &A, const double *origins, const double *xforms,
+                        cudaStream_t s) {
+    CallArgs<CAP> K;
+    const int nex = A.b.nexamples;
+    K.nex = nex;
+    K.has_xf = xforms != nullptr;
+    memcpy(K.v, origins, sizeof(double) * 3 * nex);
+    if (xforms) memcpy(K.v + 3 * nex, xforms, sizeof(double) * 15 * nex);
+    const int n = std::max(std::max(A.b.nitems, A.b.natoms),
+                           std::max(3 * nex, nex * (A.b.nchannels + 1)));
+    if (n > 0) {
+        k_prepare_static<CAP><<<(n + 255) / 256, 256, 0, s>>>(A, K);
+        LAUNCH_CHECK();
+    }
+    return GM_OK;
 }
 
 // One CTA per example, in phases separated by CTA barriers:
@@ -164,7 +246,6 @@ __global__ void __launch_bounds__(1024) k_prepare_example(const PrepArgs A) {
     int *rank = chs + n;
     int *tab = rank + n;  // [nchunk][C]
     int *off = tab + nchunk * C;
-    int *crank = off + C + 1;  // [C]
     for (int t = threadIdx.x; t < nchunk * C; t += blockDim.x) tab[t] = 0;
     if (vector) {  // positions of all atoms (items only see atoms that have weights)
         for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < b.natoms;
@@ -210,26 +291,13 @@ __global__ void __launch_bounds__(1024) k_prepare_example(const PrepArgs A) {
     }
     __syncthreads();
     if (warp == 0) {
-        // The forward's job table: channels by item count, descending (ties by
-        // channel), so it schedules the heaviest tiles first and ends on the
-        // cheap ones; each entry carries the channel's item range.
-        int4 *jobs = A.ws.chan_job + (size_t)e * C;
+        // channel offsets: exclusive scan of the counts, 32 channels per pass
         int32_t *co = A.ws.chan_off + (size_t)e * (C + 1);
-        for (int c = lane; c < C; c += 32) {
-            const int k = off[c];
-            int rk = 0;
-            for (int q = 0; q < C; q++) {
-                const int kq = off[q];
-                rk += (kq > k) || (kq == k && q < c);
-            }
-            crank[c] = rk;
-        }
-        __syncwarp();
         int pos = is;
         for (int c0 = 0; c0 < C; c0 += 32) {
             const int c = c0 + lane;
             const int k = c < C ? off[c] : 0;
-            int sc = k;  // inclusive scan of the counts
+            int sc = k;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int t = __shfl_up_sync(0xffffffffu, sc, o);
@@ -237,10 +305,8 @@ __global__ void __launch_bounds__(1024) k_prepare_example(const PrepArgs A) {
             }
             __syncwarp();
             if (c < C) {
-                const int st = pos + sc - k;
-                off[c] = st;
-                co[c] = st;
-                jobs[crank[c]] = make_int4(c, st, st + k, 0);
+                off[c] = pos + sc - k;
+                co[c] = pos + sc - k;
             }
             pos += __shfl_sync(0xffffffffu, sc, 31);
         }
@@ -279,7 +345,7 @@ gm_status prepare_impl(const gm_params *p, const gm_batch *b, const Workspace &w
     }
     if (b->max_example_items < 0) return gm_fail(GM_ERR_INVALID, "max_example_items < 0");
     const size_t n = (size_t)b->max_example_items, nchunk = (n + 31) / 32;
-    const size_t base = sizeof(int) * (2 * n + nchunk * b->nchannels + 2 * b->nchannels + 1);
+    const size_t base = sizeof(int) * (2 * n + nchunk * b->nchannels + b->nchannels + 1);
     const size_t staged = base + n * (sizeof(FwdItem) + (p->binary ? sizeof(BinItem) : 0));
     const size_t limit = 200 * 1024;
     if (base > limit)
@@ -293,4 +359,18 @@ gm_status prepare_impl(const gm_params *p, const gm_batch *b, const Workspace &w
     }
     LAUNCH_CHECK();
     return GM_OK;
+}
+
+// Per-call arrays from host memory (see gm_prepare_inline).
+gm_status prepare_inline_impl(const gm_params *p, const gm_batch *b, const Workspace &ws,
+                              const double *origins, const double *xforms, cudaStream_t s) {
+    PrepArgs A;
+    A.p = *p;
+    A.b = *b;
+    A.ws = ws;
+    A.eg = exp((-2.0 * p->gaussian_radius_multiple) * p->gaussian_radius_multiple);
+    const int nex = b->nexamples;
+    if (nex <= 8) return launch_static<8>(A, origins, xforms, s);
+    if (nex <= 64) return launch_static<64>(A, origins, xforms, s);
+    return launch_static<GM_INLINE_MAX_EXAMPLES>(A, origins, xforms, s);
 }

@@ -159,6 +159,25 @@ class PackedBatch:
         self.max_example_items = int((ex_end - ex_start).max()) if self.nexamples else 0
         L.add("ex_item_start", ex_start)
         L.add("ex_item_end", ex_end)
+        # static grouping (gm_batch.item_perm / chan_off): per example, items in
+        # (output channel, item) order -- the forward's per-channel item lists
+        # in the reference's accumulation order, computed once per batch
+        if self.vector_mode:
+            ia = L.arrays[[n for n, _ in L.arrays].index("item_atom")][1].astype(np.int64)
+            ich = L.arrays[[n for n, _ in L.arrays].index("item_channel")][1].astype(np.int64)
+            iset = atom_set[ia]
+            chan = set_choff[iset].astype(np.int64) + ich
+        else:
+            iset = atom_set
+            chan = set_choff[iset].astype(np.int64) + atom_type.astype(np.int64)
+        C = max(self.nchannels, 1)
+        key = set_example[iset].astype(np.int64) * C + chan if self.nitems else np.zeros(0, np.int64)
+        perm = np.argsort(key, kind="stable").astype(np.int32)
+        bounds = np.arange(self.nexamples, dtype=np.int64)[:, None] * C + \
+            np.arange(self.nchannels + 1, dtype=np.int64)[None, :]
+        chan_off = np.searchsorted(key[perm], bounds.reshape(-1), side="left").astype(np.int32)
+        L.add("item_perm", perm)
+        L.add("chan_off", chan_off)
         self.offsets = L.offsets
 
         # one pinned staging buffer -> one device buffer
@@ -177,6 +196,7 @@ class PackedBatch:
         self.default_centers = np.stack([_default_center(sets) for sets in example_sets]) \
             if self.nexamples else np.zeros((0, 3))
         self._percall = None
+        self._stage = None
         self._gm = None
         self._gm_ref = None
 
@@ -205,6 +225,7 @@ class PackedBatch:
         cuda = self.device.type == "cuda"
         if self._percall is None:
             self._percall = torch.empty(max(18 * n, 1), dtype=torch.float64, device=self.device)
+        if self._stage is None:
             self._stage = [torch.empty(max(18 * n, 1), dtype=torch.float64, pin_memory=cuda)
                            for _ in range(3)]
             self._stage_ev = [None, None, None]
@@ -229,6 +250,17 @@ class PackedBatch:
         if self._gm is not None:
             self._gm.xforms = self._percall.data_ptr() + 8 * 3 * n if self._has_xforms else None
 
+    def ensure_call_buffer(self, has_xforms: bool) -> None:
+        """Allocate the device per-call buffer without staging anything (the
+        inline prepare path fills the origins from the launch itself)."""
+        if self._percall is None:
+            self._percall = torch.empty(max(18 * self.nexamples, 1), dtype=torch.float64,
+                                        device=self.device)
+        self._has_xforms = bool(has_xforms)
+        if self._gm is not None:
+            self._gm.xforms = (self._percall.data_ptr() + 8 * 3 * self.nexamples
+                               if self._has_xforms else None)
+
     def gm_batch(self) -> _native.GmBatch:
         """The C-ABI batch descriptor (built once; pointers are stable)."""
         if self._percall is None:
@@ -243,7 +275,8 @@ class PackedBatch:
             for name in ("coords32", "atom_radius", "atom_set", "atom_type", "set_start",
                          "set_end", "set_example", "set_choff", "set_t", "set_wstart", "weights",
                          "type_radius", "set_trstart", "item_atom", "item_channel",
-                         "item_weight", "item_radius", "ex_item_start", "ex_item_end"):
+                         "item_weight", "item_radius", "ex_item_start", "ex_item_end",
+                         "item_perm", "chan_off"):
                 setattr(b, name, self.ptr(name))
             base = self._percall.data_ptr()
             b.origins = base

@@ -229,8 +229,20 @@ class GridMaker:
                 xforms = np.stack([t.packed() if isinstance(t, geom.Transform)
                                    else np.asarray(t, np.float64).reshape(15)
                                    for t in transforms]) if len(transforms) else np.zeros((0, 15))
-        pb.set_call_arrays(origins, xforms)
         p = self._gm_params(npts)
+        if pb.nexamples <= _native.INLINE_MAX_EXAMPLES:
+            # per-call arrays travel inside the prepare launch (no copy)
+            pb.ensure_call_buffer(xforms is not None)
+            b = pb.gm_batch()
+            org = np.ascontiguousarray(origins, np.float64)
+            xf = None if xforms is None else np.ascontiguousarray(xforms, np.float64)
+            with torch.cuda.device(pb.device):
+                _native.check(_native.lib().gm_prepare_inline(
+                    ctypes.byref(p), ctypes.byref(b), pb.workspace.data_ptr(),
+                    pb.workspace_bytes, org.ctypes.data, None if xf is None else xf.ctypes.data,
+                    stream_handle(pb.device)))
+            return p
+        pb.set_call_arrays(origins, xforms)
         b = pb.gm_batch()
         with torch.cuda.device(pb.device):
             _native.check(_native.lib().gm_prepare(
