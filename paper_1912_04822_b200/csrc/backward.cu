@@ -32,6 +32,7 @@ struct BwdArgs {
     float *coord_grad;
     float *type_grad;
     const FwdItem *items;  // index mode: item a == atom a; its box (cut rmult*r) is reused
+    const BwdAtom *batoms; // index mode: per-atom records of the prepare pass
     double eg;             // exp(-2 grm^2), a batch constant (_kernels.py:224)
 };
 
@@ -300,31 +301,29 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
     const gm_batch &b = P.b;
     if (a >= b.natoms) return;
     const int D = P.p.npts;
-    const double res = P.p.resolution, grm = P.p.gaussian_radius_multiple;
+    const double res = P.p.resolution;
     const float inv_res = (float)(1.0 / res);
+    // the prepare pass's record: position relative to the origin, constants,
+    // and the forward item's box (_kernels.py:225-227) -- one load level
+    const BwdAtom W = P.batoms[a];
     Atom A;
-    int s, e;
-    load_atom(P, a, A, s, e);
-    const int c = b.set_choff[s] + b.atom_type[a];
-    const double r = b.atom_radius[a];
-    const double d0 = grm * r, d02 = d0 * d0;
-    const double q0 = (2.0 * grm) / r;
-    const double qa2 = 2.0 * (P.eg * (q0 * q0));
-    const double m4inv_r2 = -4.0 / (r * r);
-    // the forward item of this atom carries the same box (_kernels.py:225-227)
-    const int4 bx = *reinterpret_cast<const int4 *>(&P.items[a].ibox);
-    A.dzr = P.p.radius_multiple * r;
-    A.dzr2 = A.dzr * A.dzr;
-    A.m2inv_r2 = 0.5 * m4inv_r2;
-    A.i0 = box_lo(bx.x);
-    A.i1 = box_hi(bx.x);
-    A.j0 = box_lo(bx.y);
-    A.j1 = box_hi(bx.y);
-    A.k0 = box_lo(bx.z);
-    A.k1 = box_hi(bx.z);
+    A.x = W.lx;
+    A.y = W.ly;
+    A.z = W.lz;
+    A.ox = A.oy = A.oz = 0.0;
+    A.dzr = W.dzr;
+    A.dzr2 = W.dzr2;
+    A.m2inv_r2 = W.m2inv_r2;
+    A.i0 = box_lo(W.ibox);
+    A.i1 = box_hi(W.ibox);
+    A.j0 = box_lo(W.jbox);
+    A.j1 = box_hi(W.jbox);
+    A.k0 = box_lo(W.kbox);
+    A.k1 = box_hi(W.kbox);
+    const double d02 = W.d02, qa2 = W.qa2, m4inv_r2 = W.m4inv_r2;
     double g0x = 0.0, g0y = 0.0, g0z = 0.0, g1x = 0.0, g1y = 0.0, g1z = 0.0;
     if (A.i0 <= A.i1 && A.j0 <= A.j1 && A.k0 <= A.k1) {
-        const float *gbase = P.grid_grad + ((size_t)e * b.nchannels + c) * ((size_t)D * D * D);
+        const float *gbase = P.grid_grad + (size_t)W.slab * ((size_t)D * D * D);
         const double dzr = A.dzr, dzr2 = A.dzr2;
         const double qa2dzr = qa2 * dzr;
         flat_walk<true>(A, wsm[warp], gbase, D, res, inv_res, lane, m4inv_r2,
@@ -488,6 +487,7 @@ gm_status backward_impl(const gm_params *p, const gm_batch *b, const Workspace &
     P.coord_grad = coord_grad;
     P.type_grad = type_grad;
     P.items = ws.items;
+    P.batoms = ws.batoms;
     P.eg = exp((-2.0 * p->gaussian_radius_multiple) * p->gaussian_radius_multiple);
     if (b->vector_mode)
         k_backward_vector<<<(b->natoms + kBwdWarps - 1) / kBwdWarps, kBwdWarps * 32, 0, s>>>(P);

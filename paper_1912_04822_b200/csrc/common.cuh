@@ -59,6 +59,18 @@ struct __align__(16) BinItem {
     double x, y, z, r2;
 };
 
+// Index-mode backward record of one atom, written by the prepare pass so the
+// backward starts from one independent 16-B-load level.
+struct __align__(16) BwdAtom {
+    double lx, ly, lz;       // transformed position minus the example's origin
+    double dzr, dzr2, d02;   // cutoff rmult*r and its square, (grm r)^2
+    double qa2, m4inv_r2;    // 2 qa (_kernels.py:224 tail slope), -4 / r^2
+    double m2inv_r2, pad;    // -2 / r^2 (per-axis Gaussian tables)
+    int slab;                // e * nchannels + channel: the atom's grid_grad block
+    int ibox, jbox, kbox;    // voxel box (lo | hi << 16); ibox lo > hi if it misses
+};
+static_assert(sizeof(BwdAtom) == 96, "BwdAtom must be 96 bytes");
+
 __host__ __device__ inline int box_lo(int b) { return b & 0xffff; }
 __host__ __device__ inline int box_hi(int b) { return b >> 16; }
 
@@ -74,6 +86,7 @@ struct Workspace {
     BinItem *bsorted;    // nitems (binary mode)
     int2 *sbox;          // nitems: {ibox, jbox} of sorted items (forward culling)
     int32_t *chan_off;   // nexamples * (nchannels + 1): ranges into sorted
+    BwdAtom *batoms;     // natoms (index mode): backward records
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -98,6 +111,7 @@ inline size_t carve_workspace(void *base, int32_t natoms, int32_t nitems, int32_
     ws->bsorted = (BinItem *)take(sizeof(BinItem) * ni);
     ws->sbox = (int2 *)take(sizeof(int2) * ni);
     ws->chan_off = (int32_t *)take(sizeof(int32_t) * (size_t)std::max(nex, 1) * (nch + 1));
+    ws->batoms = (BwdAtom *)take(sizeof(BwdAtom) * na);
     return off + 256;
 }
 

@@ -137,6 +137,33 @@ __device__ __forceinline__ int make_item_o(const PrepArgs &A, int it, int a, int
     return valid ? ch : -1;
 }
 
+// Index mode: the backward's per-atom record (same box as the forward item,
+// _kernels.py:225-227; constants of _kernels.py:224-251).
+__device__ __forceinline__ void store_bwd_atom(const PrepArgs &A, int a, int e, int ch,
+                                               const double *O, const double x[3],
+                                               const FwdItem &f) {
+    const double r = A.b.atom_radius[a];
+    const double grm = A.p.gaussian_radius_multiple;
+    BwdAtom w;
+    w.lx = x[0] - O[0];
+    w.ly = x[1] - O[1];
+    w.lz = x[2] - O[2];
+    w.dzr = A.p.radius_multiple * r;
+    w.dzr2 = w.dzr * w.dzr;
+    const double d0 = grm * r;
+    w.d02 = d0 * d0;
+    const double q0 = (2.0 * grm) / r;
+    w.qa2 = 2.0 * (A.eg * (q0 * q0));
+    w.m4inv_r2 = -4.0 / (r * r);
+    w.m2inv_r2 = 0.5 * w.m4inv_r2;
+    w.pad = 0.0;
+    w.slab = e * A.b.nchannels + ch;
+    w.ibox = f.ibox;
+    w.jbox = f.jbox;
+    w.kbox = f.kbox;
+    A.ws.batoms[a] = w;
+}
+
 __device__ __forceinline__ int make_item(const PrepArgs &A, int it, int a, const double x3[3],
                                          FwdItem &f, BinItem &bi) {
     const int s = A.b.atom_set[a];
@@ -183,6 +210,7 @@ __global__ void __launch_bounds__(256) k_prepare_static(const PrepArgs A, const 
         FwdItem f;
         BinItem bi;
         if (make_item_o(A, it, a, s, K.v + 3 * e, x, f, bi) < 0) f.ibox = 0x7fff;  // empty
+        if (!vector) store_bwd_atom(A, a, e, f.ch, K.v + 3 * e, x, f);
         A.ws.sorted[t] = f;
         A.ws.sbox[t] = make_int2(f.ibox, f.jbox);
         if (A.p.binary) A.ws.bsorted[t] = bi;
@@ -264,6 +292,13 @@ __global__ void __launch_bounds__(1024) k_prepare_example(const PrepArgs A) {
         FwdItem f;
         BinItem bi;
         chs[q] = make_item(A, it, a, x, f, bi);
+        if (!vector) {
+            FwdItem g = f;
+            if (chs[q] < 0) g.ibox = 0x7fff;
+            const int s = b.atom_set[a];
+            const int ex = b.set_example[s];
+            store_bwd_atom(A, a, ex, f.ch, b.origins + 3 * (size_t)ex, x, g);
+        }
         A.ws.items[it] = f;  // packed order: the index-mode backward reads its boxes
         if (SMEM_STAGE) stage[q] = f;
         if (binary) bstage[q] = bi;
