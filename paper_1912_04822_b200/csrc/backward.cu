@@ -74,6 +74,15 @@ __device__ __forceinline__ double rsqrt_d(double d2) {
 // XU, the backward's bottleneck).  Zeros and denormals map to signed zero
 // (grid gradients below 1e-38 contribute nothing at f32 output precision);
 // inf / NaN are not expected in gradients.
+// Masked variant: 0.0 unless `keep` -- branch-free (two extra LOPs).
+__device__ __forceinline__ double widen_if(float f, bool keep) {
+    const unsigned u = __float_as_uint(f);
+    const unsigned m = ((u & 0x7f800000u) != 0u && keep) ? 0xffffffffu : 0u;
+    const unsigned hi = ((u & 0x80000000u) | (((u >> 3) & 0x0fffffffu) + (896u << 20))) & m;
+    const unsigned lo = (u << 29) & m;
+    return __hiloint2double((int)hi, (int)lo);
+}
+
 __device__ __forceinline__ double widen(float f) {
     const unsigned u = __float_as_uint(f);
     const bool nz = (u & 0x7f800000u) != 0u;
@@ -294,61 +303,164 @@ __device__ __forceinline__ void flat_walk(const Atom &A, WarpBwd &W, const float
             }
 }
 
+// ---------------------------------------------------------------------------
+// Index types: the same flattened walk, specialised.  Row records carry the
+// f64 row constants (dx, dy, b2 = dx^2 + dy^2, Ex Ey (-4/r^2)) and the grid
+// offset; phase 2 is branch-free: voxels past the end of the list clamp their
+// addresses to the last voxel and contribute zero, so every lane issues the
+// same instruction stream (loads for all kU windows first, then the math).
+// ---------------------------------------------------------------------------
+struct __align__(16) IRow {
+    double dx, dy;   // row offsets x - (o + i res), y - (o + j res)
+    double b2, exy;  // dx^2 + dy^2; Ex Ey (-4 / r^2)
+    const float *gp; // grid_grad address of the row's voxel v, minus v
+    int kz;          // table index of voxel v, minus v
+    int pad;
+};
+static_assert(sizeof(IRow) == 48, "IRow must be 48 bytes");
+
+struct WarpIdx {
+    double2 zt[kTab];  // per k: offset z - (o + k res), Gaussian factor Ez
+    double dx[kTab], ex[kTab], dy[kTab], ey[kTab];
+    IRow rows[kRows];
+    unsigned starts[kRows * kTab / 32 + kU];  // bit v: a row starts at flattened voxel v
+};
+
 __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(const BwdArgs P) {
-    __shared__ WarpBwd wsm[kBwdWarps];
+    __shared__ WarpIdx wsm[kBwdWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int a = blockIdx.x * kBwdWarps + warp;
-    const gm_batch &b = P.b;
-    if (a >= b.natoms) return;
+    if (a >= P.b.natoms) return;
+    WarpIdx &W = wsm[warp];
     const int D = P.p.npts;
     const double res = P.p.resolution;
     const float inv_res = (float)(1.0 / res);
     // the prepare pass's record: position relative to the origin, constants,
     // and the forward item's box (_kernels.py:225-227) -- one load level
-    const BwdAtom W = P.batoms[a];
-    Atom A;
-    A.x = W.lx;
-    A.y = W.ly;
-    A.z = W.lz;
-    A.ox = A.oy = A.oz = 0.0;
-    A.dzr = W.dzr;
-    A.dzr2 = W.dzr2;
-    A.m2inv_r2 = W.m2inv_r2;
-    A.i0 = box_lo(W.ibox);
-    A.i1 = box_hi(W.ibox);
-    A.j0 = box_lo(W.jbox);
-    A.j1 = box_hi(W.jbox);
-    A.k0 = box_lo(W.kbox);
-    A.k1 = box_hi(W.kbox);
-    const double d02 = W.d02, qa2 = W.qa2, m4inv_r2 = W.m4inv_r2;
-    double g0x = 0.0, g0y = 0.0, g0z = 0.0, g1x = 0.0, g1y = 0.0, g1z = 0.0;
-    if (A.i0 <= A.i1 && A.j0 <= A.j1 && A.k0 <= A.k1) {
-        const float *gbase = P.grid_grad + (size_t)W.slab * ((size_t)D * D * D);
-        const double dzr = A.dzr, dzr2 = A.dzr2;
-        const double qa2dzr = qa2 * dzr;
-        flat_walk<true>(A, wsm[warp], gbase, D, res, inv_res, lane, m4inv_r2,
-                        [&](int slot, double d2, const RowEntry &R, double dz, double ez, size_t,
-                            float g) {
-                            // slope/d: Gaussian exp(-2d^2/r^2)(-4/r^2) (separable factors);
-                            // tail 2 qa (d - dzr) / d (_kernels.py:244-251)
-                            const bool in = d2 > 0.0 && d2 < dzr2;
-                            const double gv = in ? widen(g) : 0.0;
-                            const double rd = rsqrt_d(d2);
-                            // R.exy carries -4/r^2: Gaussian factor Ex Ey Ez (-4/r^2)
-                            const double t = d2 <= d02 ? R.exy * ez : fma(-qa2dzr, rd, qa2);
-                            const double scl = gv * t;
-                            if (slot) {
-                                g1x = fma(scl, R.dx, g1x);
-                                g1y = fma(scl, R.dy, g1y);
-                                g1z = fma(scl, dz, g1z);
-                            } else {
-                                g0x = fma(scl, R.dx, g0x);
-                                g0y = fma(scl, R.dy, g0y);
-                                g0z = fma(scl, dz, g0z);
+    const BwdAtom B = P.batoms[a];
+    const int i0 = box_lo(B.ibox), i1 = box_hi(B.ibox), j0 = box_lo(B.jbox),
+              j1 = box_hi(B.jbox), k0 = box_lo(B.kbox), k1 = box_hi(B.kbox);
+    const double dzr = B.dzr, dzr2 = B.dzr2, d02 = B.d02, qa2 = B.qa2;
+    const double qa2dzr = qa2 * dzr;
+    double gx = 0.0, gy = 0.0, gz = 0.0;
+    if (i0 <= i1 && j0 <= j1 && k0 <= k1) {
+        const float *gbase = P.grid_grad + (size_t)B.slab * ((size_t)D * D * D);
+        const unsigned lt = (1u << lane) - 1u, le = 0xffffffffu >> (31 - lane);
+        for (int si = i0; si <= i1; si += kTab)
+            for (int sj = j0; sj <= j1; sj += kTab)
+                for (int sk = k0; sk <= k1; sk += kTab) {
+                    const int ni = min(kTab, i1 - si + 1), nj = min(kTab, j1 - sj + 1),
+                              nk = min(kTab, k1 - sk + 1);
+                    __syncwarp();
+                    // per-axis tables: offsets (_kernels.py:232-236) and Gaussian factors
+                    for (int l = lane; l < ni + nj + nk; l += 32) {
+                        const int ax = l < ni ? 0 : (l < ni + nj ? 1 : 2);
+                        const int q = l - (ax == 0 ? 0 : (ax == 1 ? ni : ni + nj));
+                        const double d = ax == 0 ? offs(B.lx, 0.0, si + q, res)
+                                                 : (ax == 1 ? offs(B.ly, 0.0, sj + q, res)
+                                                            : offs(B.lz, 0.0, sk + q, res));
+                        const double E = exp(B.m2inv_r2 * (d * d));
+                        if (ax == 2) {
+                            W.zt[q] = make_double2(d, E);
+                        } else {
+                            (ax == 0 ? W.dx : W.dy)[q] = d;
+                            (ax == 0 ? W.ex : W.ey)[q] = E;
+                        }
+                    }
+                    __syncwarp();
+                    const float dz0 = (float)W.zt[0].x;
+                    const float inv_nj = __frcp_rn((float)nj);
+                    const unsigned sbase = (unsigned)((si * D + sj) * D + sk);
+                    const int nrows_all = ni * nj;
+                    for (int rb = 0; rb < nrows_all; rb += kRows) {
+                        // ---- phase 1: row spans, compacted with a warp scan ----
+                        int nrow = 0, total = 0;
+                        const int rend = min(nrows_all, rb + kRows);
+                        const int nwords = ((rend - rb) * nk + 31) >> 5;
+                        for (int w = lane; w < nwords + kU; w += 32) W.starts[w] = 0u;
+                        __syncwarp();
+                        for (int r0 = rb; r0 < rend; r0 += 32) {
+                            const int row = r0 + lane;
+                            int len = 0, klo = 0;
+                            const int ii = idiv(row, inv_nj), jj = row - ii * nj;
+                            double dx = 0.0, dy = 0.0, b2 = 0.0;
+                            if (row < rend) {
+                                dx = W.dx[ii];
+                                dy = W.dy[jj];
+                                b2 = fma(dy, dy, dx * dx);
+                                const double rem = dzr2 - b2;
+                                if (rem > 0.0) {
+                                    const float rho = fmaf(approx_sqrt((float)rem), 1.0001f,
+                                                           1e-5f * (float)dzr);
+                                    klo = max(0, __float2int_ru(fmaxf((dz0 - rho) * inv_res, -1.0f)));
+                                    const int khi = min(nk - 1, __float2int_rd(fminf(
+                                                                    (dz0 + rho) * inv_res, (float)nk)));
+                                    len = max(0, khi - klo + 1);
+                                }
                             }
-                        });
+                            int sc = len;  // inclusive scan of the span lengths
+#pragma unroll
+                            for (int o = 1; o < 32; o <<= 1) {
+                                const int t = __shfl_up_sync(0xffffffffu, sc, o);
+                                if (lane >= o) sc += t;
+                            }
+                            const unsigned m = __ballot_sync(0xffffffffu, len > 0);
+                            if (len > 0) {
+                                IRow &R = W.rows[nrow + __popc(m & lt)];
+                                const int st = total + sc - len;
+                                atomicOr(&W.starts[st >> 5], 1u << (st & 31));
+                                R.dx = dx;
+                                R.dy = dy;
+                                R.b2 = b2;
+                                R.exy = (W.ex[ii] * W.ey[jj]) * B.m4inv_r2;
+                                R.gp = gbase + (sbase + (unsigned)((ii * D + jj) * D + klo)) - st;
+                                R.kz = klo - st;
+                            }
+                            nrow += __popc(m);
+                            total += __shfl_sync(0xffffffffu, sc, 31);
+                        }
+                        __syncwarp();
+                        // ---- phase 2: kU windows of 32 voxels per step ----
+                        int cur = -1;  // rows started before the next window, minus one
+                        const int last = total - 1;
+                        for (int base = 0; base < total; base += 32 * kU) {
+                            int myrow[kU];
+#pragma unroll
+                            for (int u = 0; u < kU; u++) {
+                                const unsigned M = W.starts[(base >> 5) + u];
+                                myrow[u] = cur + __popc(M & le);
+                                cur += __popc(M);
+                            }
+                            float g[kU];
+#pragma unroll
+                            for (int u = 0; u < kU; u++) {
+                                const int v = min(base + 32 * u + lane, last);
+                                g[u] = __ldg(W.rows[myrow[u]].gp + v);
+                            }
+#pragma unroll
+                            for (int u = 0; u < kU; u++) {
+                                const int vr = base + 32 * u + lane;
+                                const int v = min(vr, last);
+                                const IRow &R = W.rows[myrow[u]];
+                                const double2 zt = W.zt[R.kz + v];
+                                const double dz = zt.x;
+                                const double d2 = fma(dz, dz, R.b2);
+                                const double rd = rsqrt_d(d2);
+                                // slope/d (_kernels.py:244-251): Gaussian core
+                                // Ex Ey Ez (-4/r^2), tail 2 qa (d - dzr) / d; d2 = 0
+                                // takes the core branch and contributes 0 (dx=dy=dz=0)
+                                const double t = d2 <= d02 ? R.exy * zt.y : fma(-qa2dzr, rd, qa2);
+                                const double scl = widen_if(g[u], vr <= last && d2 < dzr2) * t;
+                                gx = fma(scl, R.dx, gx);
+                                gy = fma(scl, R.dy, gy);
+                                gz = fma(scl, dz, gz);
+                            }
+                        }
+                        __syncwarp();
+                    }
+                }
     }
-    store_coord(P, a, lane, g0x + g1x, g0y + g1y, g0z + g1z);
+    store_coord(P, a, lane, gx, gy, gz);
 }
 
 // Vector types (_kernels.py:258-314).  With per-atom radii and <= kMaxT

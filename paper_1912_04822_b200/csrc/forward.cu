@@ -19,7 +19,9 @@
 // Regions are disjoint and each warp adds its items in order, so every voxel
 // is summed in the reference's item order without atomics.  The finished tile
 // (zeros included) leaves through TMA bulk stores (cp.async.bulk) when
-// D % 4 == 0: the planes of a tile are contiguous in global memory.
+// D % 4 == 0: the planes of a tile are contiguous in global memory.  A
+// channel without items is written by one CTA (its tile 0) re-sending one
+// zeroed buffer over the whole slab; the slab's other CTAs exit at once.
 // Consecutive CTAs are the channels of one tile, so scatter work and the
 // stores of empty channels interleave finely (HBM keeps writing while SMs
 // compute).
@@ -33,8 +35,8 @@ namespace {
 #ifndef GM_FWD_MINB
 #define GM_FWD_MINB 16
 #endif
-#ifndef GM_FWD_ZERO_BULK
-#define GM_FWD_ZERO_BULK 1  // zero channels leave through the bulk-store path
+#ifndef GM_FWD_ZGROUP
+#define GM_FWD_ZGROUP 8  // tiles of a zero slab written by one CTA
 #endif
 #ifndef GM_FWD_BUDGET_KB
 #define GM_FWD_BUDGET_KB 10
@@ -161,21 +163,36 @@ __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs
     float *obase = A.out + ((size_t)e * A.C + c) * D * plane + (size_t)i0 * plane + (size_t)j0 * D;
     const int chunk = TJv * D;  // contiguous floats per plane of the tile (global and smem)
 
-    // no item of this channel and no bulk path: stream zeros (with the bulk
-    // path the zeroed accumulator leaves through one bulk store, which frees
-    // the CTA sooner than a loop of stores)
-    if (cs == ce && !(GM_FWD_ZERO_BULK && A.bulk)) {
-        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (A.bulk && TJv == D) {
-            // the tile's planes are one contiguous run
-            float4 *o = reinterpret_cast<float4 *>(obase);
-            const int n4 = (TIv * chunk) >> 2;
-            for (int q = tid; q < n4; q += kThreads) __stcs(o + q, z);
-        } else if (A.bulk) {
-            for (int p = 0; p < TIv; p++) {
-                float4 *o = reinterpret_cast<float4 *>(obase + p * plane);
-                for (int q = tid; q < (chunk >> 2); q += kThreads) __stcs(o + q, z);
+    if (cs == ce) {
+        // no item of this channel: the whole (example, channel) slab is zero
+        if (A.bulk) {
+            // every GM_FWD_ZGROUP-th CTA of the slab re-sends one zeroed
+            // buffer over its group of tiles (contiguous in memory) through
+            // TMA bulk stores; the other CTAs of the group leave at once
+            if (tile % GM_FWD_ZGROUP) return;
+            float4 *z4 = reinterpret_cast<float4 *>(smem);
+            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            const int nz4 = (int)(A.acc_floats >> 2);
+            for (int q = tid; q < nz4; q += kThreads) z4[q] = z;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            const int t1 = min(tile + GM_FWD_ZGROUP, (int)gridDim.y);
+            const int i1 = (t1 - 1) / A.ntj * TI, jl = ((t1 - 1) % A.ntj) * TJ;
+            // end of the last tile of the group: plane min(i1+TI, D), row band jl
+            const size_t end = min(TJ + jl, D) == D
+                                   ? (size_t)min(i1 + TI, D) * plane
+                                   : (size_t)i1 * plane + (size_t)(jl + TJ) * D;
+            float *slab = A.out + ((size_t)e * A.C + c) * D * plane;
+            const size_t begin = (size_t)i0 * plane + (size_t)j0 * D;
+            const size_t total = end - begin, per = (size_t)nz4 * 4;
+            const size_t nst = (total + per - 1) / per;
+            for (size_t q = tid; q < nst; q += kThreads) {
+                const size_t o = q * per;
+                bulk_store(slab + begin + o, reinterpret_cast<const float *>(smem),
+                           (uint32_t)(std::min(per, total - o) * 4u));
             }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         } else {
             for (int p = 0; p < TIv; p++)
                 for (int q = tid; q < chunk; q += kThreads) __stcs(obase + p * plane + q, 0.f);
@@ -292,15 +309,24 @@ __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs
                         float *ap = accp + S3.x + kk + r * D;
                         const int step = rpi * D;
                         float jf = (float)(jr0 + r);
-                        for (int jj = r; jj < nj; jj += rpi, jf += rpif, ap += step) {
-                            const float dy = RESL ? fmaf(jf, resf, S0.x) + fmaf(jf, resl, S0.y)
-                                                  : fmaf(jf, resf, S0.x) + S0.y;
+                        auto val = [&](float y) {
+                            const float dy = RESL ? fmaf(y, resf, S0.x) + fmaf(y, resl, S0.y)
+                                                  : fmaf(y, resf, S0.x) + S0.y;
                             const float d2 = fmaf(dy, dy, b2);
                             const float g = fast_ex2(d2 * cexp);
                             const float t2 = fmaxf(cut - fast_sqrt(d2), 0.0f);
-                            const float v = d2 <= d02 ? g : qa * t2 * t2;
-                            *ap = fmaf(w, v, *ap);
+                            return d2 <= d02 ? g : qa * t2 * t2;
+                        };
+                        int jj = r;
+                        // two rows per iteration: both accumulator reads are
+                        // issued before either write (different rows)
+                        for (; jj + rpi < nj; jj += 2 * rpi, jf += 2.0f * rpif, ap += 2 * step) {
+                            const float v0 = val(jf), v1 = val(jf + rpif);
+                            const float a0 = ap[0], a1 = ap[step];
+                            ap[0] = fmaf(w, v0, a0);
+                            ap[step] = fmaf(w, v1, a1);
                         }
+                        if (jj < nj) *ap = fmaf(w, val(jf), *ap);
                     }
                 } else {
                     // > 32 columns (very fine grids): one row pass per 32 columns

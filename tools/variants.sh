@@ -10,5 +10,5 @@ while [ $# -ge 2 ]; do
     -Xcompiler -fPIC,-ffp-contract=off -Xptxas -v --expt-relaxed-constexpr -I../../include \
     $flags -shared -o ../variants/$name.so abi.cu prepare.cu forward.cu backward.cu 2> ../variants/$name.log \
     || { grep -i error ../variants/$name.log; exit 1; }
-  echo "$name: $(grep -A2 'k_backward_index' ../variants/$name.log | grep -E 'Used|spill' | tr '\n' ' ')"
+  echo "$name: $(grep -A2 "${GREPK:-k_backward_index}" ../variants/$name.log | grep -E 'Used|spill' | tr '\n' ' ')"
 done
