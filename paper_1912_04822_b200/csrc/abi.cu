@@ -40,6 +40,24 @@ cudaError_t gm_ensure_smem(const void *func, int bytes) {
     return e;
 }
 
+int gm_persistent_blocks(const void *func, int threads, size_t smem) {
+    static std::mutex mu;
+    struct Entry { int dev; const void *f; int threads; size_t smem; int blocks; };
+    static std::vector<Entry> done;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto &d : done)
+        if (d.dev == dev && d.f == func && d.threads == threads && d.smem == smem) return d.blocks;
+    int sms = 0, per = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, func, threads, smem) != cudaSuccess)
+        return 0;
+    const int blocks = std::max(1, per) * sms;
+    done.push_back({dev, func, threads, smem, blocks});
+    return blocks;
+}
+
 static gm_status check_params(const gm_params *p) {
     if (!p) return gm_fail(GM_ERR_INVALID, "params is NULL");
     if (!(p->resolution > 0)) return gm_fail(GM_ERR_INVALID, "resolution must be > 0");

@@ -157,6 +157,9 @@ constexpr int kBwdWarps = GM_BWD_WARPS;
 #ifndef GM_BWD_CHAINS
 #define GM_BWD_CHAINS 1
 #endif
+#ifndef GM_BWD_F2F
+#define GM_BWD_F2F 1  // widen grid gradients with F2F (XU) instead of integer ops
+#endif
 #ifndef GM_BWD_MINB
 #define GM_BWD_MINB 32
 #endif
@@ -450,7 +453,11 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
                                 // Ex Ey Ez (-4/r^2), tail 2 qa (d - dzr) / d; d2 = 0
                                 // takes the core branch and contributes 0 (dx=dy=dz=0)
                                 const double t = d2 <= d02 ? R.exy * zt.y : fma(-qa2dzr, rd, qa2);
+#if GM_BWD_F2F
+                                const double scl = (double)((vr <= last && d2 < dzr2) ? g[u] : 0.0f) * t;
+#else
                                 const double scl = widen_if(g[u], vr <= last && d2 < dzr2) * t;
+#endif
                                 gx = fma(scl, R.dx, gx);
                                 gy = fma(scl, R.dy, gy);
                                 gz = fma(scl, dz, gz);

@@ -143,6 +143,10 @@ __device__ __forceinline__ int small_div(int a, float inv_b) {
     return (int)(((float)a + 0.5f) * inv_b);
 }
 
+// Resident CTAs per SM x SM count for a persistent launch (cached per device,
+// kernel, block size and dynamic shared memory size); 0 on failure.
+int gm_persistent_blocks(const void *func, int threads, size_t smem);
+
 // ---------------------------------------------------------------------------
 // host-side implementation entry points (used by abi.cu)
 // ---------------------------------------------------------------------------
