@@ -13,6 +13,10 @@
 
 #include "common.cuh"
 
+#ifndef GM_PREP_THREADS
+#define GM_PREP_THREADS 64  // small blocks: the ~50k item threads spread over every SM
+#endif
+
 struct PrepArgs {
     gm_params p;
     gm_batch b;
@@ -185,7 +189,7 @@ struct CallArgs {
 };
 
 template <int CAP>
-__global__ void __launch_bounds__(256) k_prepare_static(const PrepArgs A, const __grid_constant__ CallArgs<CAP> K) {
+__global__ void __launch_bounds__(GM_PREP_THREADS) k_prepare_static(const PrepArgs A, const __grid_constant__ CallArgs<CAP> K) {
     const gm_batch &b = A.b;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int nex = K.nex;
@@ -231,7 +235,7 @@ gm_status launch_static(const PrepArgs &A, const double *origins, const double *
     const int n = std::max(std::max(A.b.nitems, A.b.natoms),
                            std::max(3 * nex, nex * (A.b.nchannels + 1)));
     if (n > 0) {
-        k_prepare_static<CAP><<<(n + 255) / 256, 256, 0, s>>>(A, K);
+        k_prepare_static<CAP><<<(n + GM_PREP_THREADS - 1) / GM_PREP_THREADS, GM_PREP_THREADS, 0, s>>>(A, K);
         LAUNCH_CHECK();
     }
     return GM_OK;
