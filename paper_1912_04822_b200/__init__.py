@@ -8,7 +8,8 @@ in-tree CUDA extension (``libgridmaker_b200.so``, sm_100a) via its C ABI.
 """
 
 from .coordsets import CoordinateSet, Example, make_vector_types
-from .errors import ConfigError, DeviceError, VoxmolError
+from .errors import ConfigError, DeviceError, FormatError, VoxmolError
+from .export import read_npy, write_npy
 from .geom import (IDENTITY_QUATERNION, Quaternion, Transform, draw_transforms,
                    make_transform, random_unit_quaternion, transform_example)
 from .voxelizer import GridMaker, channel_count, channel_names, save_grid
@@ -17,7 +18,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "CoordinateSet", "Example", "make_vector_types", "ConfigError", "DeviceError",
-    "VoxmolError", "IDENTITY_QUATERNION", "Quaternion", "Transform", "draw_transforms",
+    "VoxmolError", "FormatError", "read_npy", "write_npy", "IDENTITY_QUATERNION", "Quaternion", "Transform", "draw_transforms",
     "make_transform", "random_unit_quaternion", "transform_example", "GridMaker",
     "channel_count", "channel_names", "save_grid",
 ]

@@ -3,7 +3,7 @@
 Mirrors the classes the reference raises on this path
 (/root/reference/pkg/src/voxmol/errors.py:4-33): ``ConfigError`` is raised by
 ``GridMaker`` for ``radius_type_indexed`` without a radius table
-(voxelizer.py:315).  ``DeviceError`` is ours: a CUDA launch/resource failure
+(voxelizer.py:315); ``FormatError`` by the MOLC / NPY readers.  ``DeviceError`` is ours: a CUDA launch/resource failure
 reported through the C ABI status code.
 """
 
@@ -14,6 +14,11 @@ class VoxmolError(Exception):
 
 class ConfigError(VoxmolError, ValueError):
     """Options are inconsistent with each other or with the data."""
+
+
+class FormatError(VoxmolError, ValueError):
+    """A binary container (MOLC cache, NPY file) is malformed or truncated
+    (errors.py:28-29)."""
 
 
 class DeviceError(VoxmolError, RuntimeError):

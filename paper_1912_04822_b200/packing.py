@@ -82,6 +82,8 @@ class PackedBatch:
                 radius[a0:a1] = cs.radii.astype(np.float64) * scale
             atom_set[a0:a1] = s
 
+        self.atom_example = set_example[atom_set] if self.natoms else np.zeros(0, np.int32)
+
         L = _Layout()
         L.add("coords32", coords)
         L.add("atom_radius", radius)
@@ -110,7 +112,7 @@ class PackedBatch:
             self.nitems = self.natoms
             self.nweights = 0
         else:
-            wparts, trparts, it_atom, it_ch, it_w, it_r = [], [], [], [], [], []
+            wparts, trparts, it_atom, it_ch, it_w, it_r, it_wi = [], [], [], [], [], [], []
             set_wstart = np.zeros(self.nsets, np.int32)
             set_trstart = np.zeros(self.nsets, np.int32)
             wpos = tpos = ipos = 0
@@ -139,6 +141,7 @@ class PackedBatch:
                     it_ch.append(ic.astype(np.int32))
                     it_w.append(tv[ia, ic].astype(np.float32))
                     it_r.append(tr[ic] if radius_type_indexed else radius[ia + a0])
+                    it_wi.append((wpos + ia * nt + ic).astype(np.int64))
                     ipos += ia.shape[0]
                 ex_end[e] = ipos
                 self.placed.append((e, choff, cs, a0, int(wpos)))
@@ -156,6 +159,8 @@ class PackedBatch:
             L.add("item_radius", cat(it_r, np.float64))
             self.nitems = int(ipos)
             self.nweights = int(wpos)
+            # item -> its entry of the packed weight rows (autograd weight refresh)
+            self.item_windex = cat(it_wi, np.int64)
         self.max_example_items = int((ex_end - ex_start).max()) if self.nexamples else 0
         L.add("ex_item_start", ex_start)
         L.add("ex_item_end", ex_end)
@@ -208,6 +213,34 @@ class PackedBatch:
     def upload(self, non_blocking: bool = True) -> None:
         """Copy the pinned host image to the device (one H2D copy)."""
         self.dev.copy_(self.host, non_blocking=non_blocking)
+
+    def device_view(self, name: str) -> torch.Tensor:
+        """A typed tensor view of one packed array inside the device buffer."""
+        off, dt, shape = self.offsets[name]
+        n = int(np.prod(shape)) if len(shape) else 1
+        tdt = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64,
+               np.dtype(np.int32): torch.int32}[np.dtype(dt)]
+        nbytes = n * np.dtype(dt).itemsize
+        return self.dev[off:off + nbytes].view(tdt).view(shape)
+
+    def load_coords(self, coords: torch.Tensor) -> None:
+        """Replace the packed input-frame coordinates with a (natoms, 3)
+        device tensor (a device-to-device copy, stream-ordered)."""
+        if self.natoms:
+            self.device_view("coords32").copy_(coords.detach().reshape(self.natoms, 3))
+
+    def load_weights(self, weights: torch.Tensor) -> None:
+        """Vector mode: replace the packed type weights (nweights,) and the
+        forward items' weights.  The items (nonzero pattern) are fixed at pack
+        time: entries that were zero when packed stay without a forward item."""
+        if not self.vector_mode or not self.nweights:
+            return
+        w = weights.detach().reshape(-1).to(torch.float32)
+        self.device_view("weights").copy_(w)
+        if self.nitems:
+            if getattr(self, "_item_windex_dev", None) is None:
+                self._item_windex_dev = torch.from_numpy(self.item_windex).to(self.device)
+            self.device_view("item_weight").copy_(w[self._item_windex_dev])
 
     def ptr(self, name: str) -> int | None:
         if name not in self.offsets:

@@ -27,7 +27,7 @@ import os
 import numpy as np
 import torch
 
-from . import _native, geom
+from . import _native, export, geom
 from .coordsets import coord_sets_of, is_coordinate_set
 from .errors import ConfigError, DeviceError
 from .packing import PackedBatch, stream_handle
@@ -515,8 +515,10 @@ class GridMaker:
             na, nt = int(cs.coords.shape[0]), int(cs.num_types)
             c = cg[a0:a0 + na]
             if input_frame and transforms is not None:
+                # d/dx = R^T d/dx' (row vectors: g R), in f64 then rounded once
                 R = _rotation_of(transforms[e])
-                c = c @ (torch.from_numpy(R).to(c) if as_tensor else R.astype(np.float32))
+                c = ((c.double() @ torch.from_numpy(R).to(c.device)).float() if as_tensor
+                     else (c.astype(np.float64) @ R).astype(np.float32))
             t = None
             if pb.vector_mode:
                 t = tg[w0:w0 + na * nt].reshape(na, nt)
@@ -568,28 +570,7 @@ def _check_device_in(t, shape, device, name):
 
 
 def save_grid(path, grid, origin=None, resolution=None, channel_labels=None, extra=None) -> str:
-    """NPY + JSON sidecar export (voxelizer.py:438-465); accepts CUDA tensors."""
-    path = os.fspath(path)
-    arr = _unwrap(grid)
-    if _is_tensor(arr):
-        arr = arr.detach().cpu().numpy()
-    arr = np.ascontiguousarray(arr)
-    np.save(path, arr, allow_pickle=False)
-    meta = {"shape": list(arr.shape)}
-    if resolution is not None:
-        meta["resolution"] = float(resolution)
-    if origin is not None:
-        o = np.asarray(origin, dtype=np.float64)
-        if o.ndim == 1:
-            meta["origin"] = [float(v) for v in o]
-        else:
-            meta["origins"] = [[float(v) for v in row] for row in o]
-    if channel_labels is not None:
-        meta["channels"] = list(channel_labels)
-    if extra:
-        meta.update(extra)
-    sidecar = os.path.splitext(path)[0] + ".json"
-    with open(sidecar, "w", encoding="utf-8") as fh:
-        json.dump(meta, fh, indent=2, sort_keys=True)
-        fh.write("\n")
-    return sidecar
+    """NPY + JSON sidecar export (voxelizer.py:438-465); accepts CUDA tensors
+    (streamed device -> pinned -> file, see export.py)."""
+    return export.save_grid(path, grid, origin=origin, resolution=resolution,
+                            channel_labels=channel_labels, extra=extra)

@@ -290,3 +290,21 @@ def test_packing_layout_cpu():
     np.testing.assert_allclose(tr, synthetic.TYPE_RADII[ic].astype(np.float64) * 1.1)
     np.testing.assert_array_equal(arr("set_choff"), [0, 14] * 3)
     np.testing.assert_array_equal(pb.default_centers[0], exs[0].coord_sets[1].centroid())
+
+
+def test_vector_item_windex_maps_items_to_weight_rows():
+    """PackedBatch.item_windex (autograd weight refresh) points every forward
+    item at its entry of the packed weight rows."""
+    from paper_1912_04822_b200 import synthetic
+    from paper_1912_04822_b200.packing import PackedBatch
+
+    exs = synthetic.batch(3, seed=4, vector=True)
+    pb = PackedBatch([ex.coord_sets for ex in exs], 28, True, 1.0, False, "cpu")
+    host = {}
+    for name in ("weights", "item_weight"):
+        off, dt, shape = pb.offsets[name]
+        n = int(np.prod(shape))
+        host[name] = pb.host.numpy()[off:off + n * np.dtype(dt).itemsize].view(dt)
+    assert pb.item_windex.shape == (pb.nitems,)
+    np.testing.assert_array_equal(host["weights"][pb.item_windex], host["item_weight"])
+    assert pb.atom_example.shape == (pb.natoms,)
