@@ -177,7 +177,9 @@ class PackedBatch:
             chan = set_choff[iset].astype(np.int64) + atom_type.astype(np.int64)
         C = max(self.nchannels, 1)
         key = set_example[iset].astype(np.int64) * C + chan if self.nitems else np.zeros(0, np.int64)
-        perm = np.argsort(key, kind="stable").astype(np.int32)
+        # stable sort of small keys: 16-bit keys take numpy's radix sort
+        skey = key.astype(np.int16) if self.nexamples * C < 32767 else key
+        perm = np.argsort(skey, kind="stable").astype(np.int32)
         bounds = np.arange(self.nexamples, dtype=np.int64)[:, None] * C + \
             np.arange(self.nchannels + 1, dtype=np.int64)[None, :]
         chan_off = np.searchsorted(key[perm], bounds.reshape(-1), side="left").astype(np.int32)

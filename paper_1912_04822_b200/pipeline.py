@@ -1,0 +1,113 @@
+"""Example provider -> device batch pipeline.
+
+The reference's training loop calls ``ExampleProvider.next_batch(n)``
+(/root/reference/pkg/src/voxmol/sampling.py:364-380) and hands the examples
+to ``GridMaker.forward_batch``, which packs them into CSR arrays on the host
+(voxelizer.py:372-435) every call, serially with the gridding.
+
+``DeviceBatchPipeline`` overlaps those host steps with the device: a worker
+thread pulls batches from the provider, packs them (``PackedBatch``: one
+pinned host image per batch) and uploads each with one host->device copy on
+a side stream, ``depth`` batches ahead.  The consumer gets device-resident
+``PackedBatch``es whose upload has been ordered before its own stream's
+work, ready for ``GridMaker.forward_packed`` / ``backward_packed``.
+"""
+
+from __future__ import annotations
+
+import queue
+import threading
+
+import torch
+
+
+class DeviceBatchPipeline:
+    """Iterator of device-resident packed batches.
+
+    ``source``: an object with ``next_batch(n)`` (the reference's
+    ``ExampleProvider``), or any iterable yielding lists of examples.
+    """
+
+    _DONE = object()
+
+    def __init__(self, gm, source, batch_size: int, depth: int = 2, nchannels=None,
+                 device=None, max_batches=None):
+        self.gm = gm
+        self.batch_size = int(batch_size)
+        self.nchannels = nchannels
+        self.device = torch.device(device) if device is not None else gm._device()
+        self.max_batches = max_batches
+        if hasattr(source, "next_batch"):
+            self._pull = lambda: source.next_batch(self.batch_size)
+        else:
+            it = iter(source)
+            self._pull = lambda: next(it)
+        self._q = queue.Queue(maxsize=max(1, int(depth)))
+        self._stop = threading.Event()
+        self._err = None
+        self._thread = threading.Thread(target=self._work, name="gm-batch-pipeline", daemon=True)
+        self._thread.start()
+
+    def _work(self):
+        try:
+            torch.cuda.set_device(self.device)
+            side = torch.cuda.Stream(device=self.device)
+            n = 0
+            while not self._stop.is_set():
+                if self.max_batches is not None and n >= self.max_batches:
+                    break
+                try:
+                    examples = self._pull()
+                except StopIteration:
+                    break
+                # pack on the host; the PackedBatch's device buffers come from
+                # the default stream, its upload runs on the side stream
+                with torch.cuda.stream(side):
+                    pb = self.gm.pack(examples, nchannels=self.nchannels, device=self.device)
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                pb.examples = examples
+                while not self._stop.is_set():
+                    try:
+                        self._q.put((pb, ev), timeout=0.1)
+                        break
+                    except queue.Full:
+                        continue
+                n += 1
+        except BaseException as exc:  # surfaced to the consumer
+            self._err = exc
+        finally:
+            self._q.put(self._DONE)
+
+    def __iter__(self):
+        return self
+
+    def __next__(self):
+        item = self._q.get()
+        if item is self._DONE:
+            self._q.put(self._DONE)
+            if self._err is not None:
+                raise self._err
+            raise StopIteration
+        pb, ev = item
+        cur = torch.cuda.current_stream(self.device)
+        cur.wait_event(ev)
+        # the batch's device memory was allocated under the side stream
+        pb.dev.record_stream(cur)
+        pb.workspace.record_stream(cur)
+        return pb
+
+    def close(self):
+        self._stop.set()
+        try:
+            while True:
+                self._q.get_nowait()
+        except queue.Empty:
+            pass
+        self._thread.join(timeout=5)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
