@@ -312,20 +312,27 @@ def main():
         torch.cuda.synchronize(dev)
 
     clocks = ClockSampler(local)
-    fevs = [(ev(), ev()) for _ in range(args.steps)]
-    bevs = [(ev(), ev()) for _ in range(args.steps)]
     t_start, t_end = ev(), ev()
     barrier()
     _native.launch_count(reset=True)
     clocks.start()
     t_start.record(stream)
     for k in range(args.steps):
-        step(fevs[k], bevs[k])
+        step()
     t_end.record(stream)
     barrier()
     clk = clocks.stop()
     launches = _native.launch_count()
     ms = t_start.elapsed_time(t_end) / args.steps
+    # kernel durations for the roofline: a second, instrumented pass of the
+    # same K steps (timing events between the launches would otherwise add
+    # their own gaps to the headline step time)
+    fevs = [(ev(), ev()) for _ in range(args.steps)]
+    bevs = [(ev(), ev()) for _ in range(args.steps)]
+    barrier()
+    for k in range(args.steps):
+        step(fevs[k], bevs[k])
+    barrier()
     fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in fevs)
     bwd_ms = statistics.mean(a.elapsed_time(b) for a, b in bevs)
     if ws > 1:
@@ -339,21 +346,47 @@ def main():
     # ---- e2e: public API with host inputs, D2H of the coordinate gradients ----
     e2e = None
     if not args.no_e2e:
-        host_cg = torch.empty((pb.natoms, 3), dtype=torch.float32, pin_memory=True)
+        # double-buffered inputs: the next step's atoms upload on a copy stream
+        # while this step grids, and each step's coordinate gradients read back
+        # on the copy stream once its backward is done (every step still does
+        # one full H2D of its inputs and one D2H of its result)
+        pbs = [pb, gm.pack(exs)]
+        cgs = [cg, torch.empty_like(cg)]
+        host_cg = [torch.empty((pb.natoms, 3), dtype=torch.float32, pin_memory=True)
+                   for _ in range(2)]
+        copy_s = torch.cuda.Stream(device=dev)
+        up = [torch.cuda.Event(), torch.cuda.Event()]
+        done = [torch.cuda.Event(), torch.cuda.Event()]
 
-        def e2e_step():
-            pb.upload()  # H2D of the packed atoms (pinned)
-            gm.forward_packed(pb, out, transforms=draw())
-            gm.backward_packed(pb, out, reuse_prepared=True, coord_grad=cg, type_grad=tg)
-            host_cg.copy_(cg, non_blocking=True)
+        def upload(x):
+            with torch.cuda.stream(copy_s):
+                copy_s.wait_event(done[x])  # the batch's previous step is finished
+                pbs[x].upload()             # H2D of the packed atoms (pinned)
+                up[x].record(copy_s)
 
-        for _ in range(3):
-            e2e_step()
+        def e2e_step(k, last):
+            x, y = k % 2, (k + 1) % 2
+            if not last:
+                upload(y)
+            stream.wait_event(up[x])
+            gm.forward_packed(pbs[x], out, transforms=draw())
+            gm.backward_packed(pbs[x], out, reuse_prepared=True, coord_grad=cgs[x], type_grad=tg)
+            done[x].record(stream)
+            with torch.cuda.stream(copy_s):
+                copy_s.wait_event(done[x])
+                host_cg[x].copy_(cgs[x], non_blocking=True)
+
+        def run(n):
+            upload(0)
+            for k in range(n):
+                e2e_step(k, k == n - 1)
+            stream.wait_stream(copy_s)
+
+        run(3)
         a, b = ev(), ev()
         barrier()
         a.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
+        run(args.steps)
         b.record(stream)
         barrier()
         e_ms = a.elapsed_time(b) / args.steps
@@ -365,11 +398,23 @@ def main():
             e_ms = float(t.item())
         e2e = {"value": ws * N / (e_ms / 1000.0), "unit": "grids/s",
                "h2d_bytes_per_step": pb.h2d_bytes + 8 * 18 * N,
-               "d2h_bytes_per_step": int(host_cg.numel() * 4),
+               "d2h_bytes_per_step": int(host_cg[0].numel() * 4),
                "note": "GridMaker.forward_packed/backward_packed with a pinned host->device "
-                       "upload of the atoms each step, loss 1/2|grid|^2, coordinate "
-                       "gradients read back to host"}
+                       "upload of the atoms each step (double-buffered on a copy stream, "
+                       "overlapping the previous step's gridding), loss 1/2|grid|^2, "
+                       "coordinate gradients read back to pinned host memory"}
 
+    # write-only HBM rate of this box (torch fill of the output buffer): the
+    # forward is write-dominated, so its fraction of the copy peak can exceed 1
+    fa, fb = ev(), ev()
+    for _ in range(3):
+        out.fill_(0.0)
+    fa.record(stream)
+    for _ in range(10):
+        out.fill_(0.0)
+    fb.record(stream)
+    torch.cuda.synchronize(dev)
+    fill_gbs = out.numel() * 4 / (fa.elapsed_time(fb) / 10 / 1000.0) / 1e9
     peak, peak_src = load_peak()
     achieved = fwd_b * N / (fwd_ms / 1000.0) / 1e9
     traffic = None
@@ -388,7 +433,9 @@ def main():
         "data": "synthetic",
         "config": {"workload": cfg["workload"], "global_batch": ws * N, "batch_per_gpu": N,
                    "grid": f"{C}x{D}^3", "parallelism": f"example-sharded x{ws}",
-                   "l2": "output 619 MB/step > 126 MB L2 (no flush needed)"},
+                   "l2": f"output {N * C * D ** 3 * 4 / 1e6:.0f} MB/step > 126 MB L2 (no flush needed)",
+                   "kernel_timing": "k_forward / k_backward durations from a second, "
+                                    "CUDA-event-instrumented pass of the same K steps"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel": "k_forward (prepare+forward launch pair)",
@@ -397,7 +444,9 @@ def main():
                      "bwd_gbs": bwd_b * N / (bwd_ms / 1000.0) / 1e9,
                      "step_gbs": (fwd_b + bwd_b) * N / (ms / 1000.0) / 1e9,
                      "step_frac": (fwd_b + bwd_b) * N / (ms / 1000.0) / 1e9 / peak,
-                     "footprint_F_per_grid": footprint},
+                     "footprint_F_per_grid": footprint,
+                     "fill_gbs_measured": fill_gbs,
+                     "frac_of_fill": achieved / fill_gbs},
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk,
