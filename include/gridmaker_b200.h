@@ -94,6 +94,16 @@ typedef struct {
      * one fully parallel pass. */
     const int32_t *item_perm;
     const int32_t *chan_off;
+    /* optional forward job table (device, 4 int32 per job: example * nchannels +
+     * channel, tile, static item range begin, end), built by gm_forward_jobs
+     * from the static chan_off for grids of fwd_jobs_npts points per side: only
+     * tiles of channels with items plus one job per group of zero tiles are
+     * launched (the kernel re-reads the item ranges of the prepare pass, so the
+     * table is valid after either prepare path).  NULL / 0 = one CTA per
+     * (channel, tile, example). */
+    const int32_t *fwd_jobs;
+    int32_t nfwd_jobs;
+    int32_t fwd_jobs_npts;
 } gm_batch;
 
 /* Device scratch needed by gm_prepare / gm_forward / gm_backward. */
@@ -112,6 +122,13 @@ gm_status gm_prepare(const gm_params *p, const gm_batch *b, void *workspace,
 gm_status gm_prepare_inline(const gm_params *p, const gm_batch *b, void *workspace,
                             size_t workspace_bytes, const double *origins_host,
                             const double *xforms_host, void *stream);
+/* Forward job table for a static grouping (host memory): chan_off_host is the
+ * (nexamples, nchannels+1) item ranges of gm_batch.chan_off.  Writes up to
+ * capacity jobs (4 int32 each) to jobs_out (may be NULL) and returns the job
+ * count, or -1 on invalid arguments.  Replaces the reference's dense launch over
+ * every (set, channel) (_kernels.py:40-47) by the tiles that have items. */
+int32_t gm_forward_jobs(const gm_params *p, int32_t nexamples, int32_t nchannels,
+                        const int32_t *chan_off_host, int32_t *jobs_out, int32_t capacity);
 /* out: (nexamples, nchannels, D, D, D) f32 device; every voxel is written. */
 gm_status gm_forward(const gm_params *p, const gm_batch *b, const void *workspace,
                      float *out, void *stream);

@@ -57,6 +57,7 @@ class GmBatch(ctypes.Structure):
         ("ex_item_start", _vp), ("ex_item_end", _vp), ("max_example_items", _c_int32),
         ("origins", _vp), ("xforms", _vp),
         ("item_perm", _vp), ("chan_off", _vp),
+        ("fwd_jobs", _vp), ("nfwd_jobs", _c_int32), ("fwd_jobs_npts", _c_int32),
     ]
 
 
@@ -67,7 +68,7 @@ EXPORTS = (
     "gm_workspace_bytes", "gm_prepare", "gm_prepare_inline", "gm_forward", "gm_backward", "gm_workspace_positions",
     "gm_forward_index_sets_host", "gm_forward_vector_sets_host", "gm_backward_index_host",
     "gm_backward_vector_host", "gm_last_error", "gm_version", "gm_device_count",
-    "gm_launch_count", "gm_struct_size", "gm_draw_transforms",
+    "gm_launch_count", "gm_struct_size", "gm_draw_transforms", "gm_forward_jobs",
 )
 
 
@@ -112,6 +113,8 @@ def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         _vp, _vp, _vp, _vp, _vp, _c_int64, _c_int64, _vp, _c_int64, _vp, _c_int32, _vp,
         _c_double, _c_double, _c_double]
     L.gm_backward_vector_host.restype = ctypes.c_int
+    L.gm_forward_jobs.argtypes = [P(GmParams), _c_int32, _c_int32, _vp, _vp, _c_int32]
+    L.gm_forward_jobs.restype = _c_int32
     L.gm_draw_transforms.argtypes = [_vp, _c_int64, _c_int32, _c_double, _vp, _vp]
     L.gm_draw_transforms.restype = ctypes.c_int
     L.gm_last_error.restype = ctypes.c_char_p

@@ -146,6 +146,15 @@ extern "C" gm_status gm_prepare_inline(const gm_params *p, const gm_batch *b, vo
     return prepare_impl(p, &bb, ws_of(workspace, b), s, true);
 }
 
+extern "C" int32_t gm_forward_jobs(const gm_params *p, int32_t nexamples, int32_t nchannels,
+                                   const int32_t *chan_off_host, int32_t *jobs_out,
+                                   int32_t capacity) {
+    if (check_params(p) != GM_OK || nexamples < 0 || nchannels < 0 || capacity < 0 ||
+        (nexamples > 0 && !chan_off_host))
+        return -1;
+    return forward_jobs_impl(p, nexamples, nchannels, chan_off_host, jobs_out, capacity);
+}
+
 extern "C" gm_status gm_forward(const gm_params *p, const gm_batch *b, const void *workspace,
                                 float *out, void *stream) {
     gm_status st = check_params(p);

@@ -156,6 +156,8 @@ gm_status prepare_inline_impl(const gm_params *p, const gm_batch *b, const Works
                               const double *origins, const double *xforms, cudaStream_t s);
 gm_status forward_impl(const gm_params *p, const gm_batch *b, const Workspace &ws, float *out,
                        cudaStream_t s);
+int32_t forward_jobs_impl(const gm_params *p, int32_t nex, int32_t nch, const int32_t *chan_off,
+                          int32_t *jobs, int32_t cap);
 gm_status backward_impl(const gm_params *p, const gm_batch *b, const Workspace &ws,
                         const float *grid_grad, float *coord_grad, float *type_grad,
                         cudaStream_t s);

@@ -53,7 +53,9 @@ struct FwdArgs {
     float *out;
     double res;
     float resf, resl, inv_res;  // res = resf + resl
+    const int4 *jobs;  // optional job table (gm_batch.fwd_jobs) or NULL
     int D, C, TI, TJ, ntj, wpp, rpw;
+    int ntiles;        // tiles per (example, channel) slab
     int bulk;
     size_t acc_floats;
 };
@@ -152,10 +154,22 @@ __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs
     // grid (channel, tile, example): consecutive CTAs are the channels of one
     // tile, so scatter work and zero-tile stores interleave finely, which
     // keeps HBM writing while SMs compute
-    const int tile = blockIdx.y, e = blockIdx.z, rank = blockIdx.x;  // rank = channel
-    const int c = rank;
-    const int cs = A.chan_off[(size_t)e * (A.C + 1) + c];
-    const int ce = A.chan_off[(size_t)e * (A.C + 1) + c + 1];
+    int tile, e, c, cs, ce;
+    if (A.jobs) {
+        // job table: only tiles with items, one job per group of zero tiles.
+        // The item range is re-read from the prepare pass (a static channel
+        // with items may still lose them all to the grid's bounds).
+        const int2 j = *reinterpret_cast<const int2 *>(A.jobs + blockIdx.x);
+        e = j.x / A.C;
+        c = j.x - e * A.C;
+        tile = j.y;
+    } else {
+        tile = blockIdx.y;
+        e = blockIdx.z;
+        c = blockIdx.x;
+    }
+    cs = A.chan_off[(size_t)e * (A.C + 1) + c];
+    ce = A.chan_off[(size_t)e * (A.C + 1) + c + 1];
     const int D = A.D, TI = A.TI, TJ = A.TJ;
     const int i0 = (tile / A.ntj) * TI, j0 = (tile % A.ntj) * TJ;
     const int TIv = min(TI, D - i0), TJv = min(TJ, D - j0);
@@ -164,27 +178,28 @@ __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs
     const int chunk = TJv * D;  // contiguous floats per plane of the tile (global and smem)
 
     if (cs == ce) {
-        // no item of this channel: the whole (example, channel) slab is zero
+        // no item of this channel: the whole (example, channel) slab is zero.
+        // Every GM_FWD_ZGROUP-th CTA of the slab writes its group of tiles
+        // (contiguous in memory); the other CTAs of the group leave at once
+        // (the job table does not even launch them).
+        if (tile % GM_FWD_ZGROUP) return;
+        const int t1 = min(tile + GM_FWD_ZGROUP, A.ntiles);
+        const int i1 = (t1 - 1) / A.ntj * TI, jl = ((t1 - 1) % A.ntj) * TJ;
+        // end of the last tile of the group: plane min(i1+TI, D), row band jl
+        const size_t end = min(TJ + jl, D) == D ? (size_t)min(i1 + TI, D) * plane
+                                                : (size_t)i1 * plane + (size_t)(jl + TJ) * D;
+        float *slab = A.out + ((size_t)e * A.C + c) * D * plane;
+        const size_t begin = (size_t)i0 * plane + (size_t)j0 * D;
+        const size_t total = end - begin;
         if (A.bulk) {
-            // every GM_FWD_ZGROUP-th CTA of the slab re-sends one zeroed
-            // buffer over its group of tiles (contiguous in memory) through
-            // TMA bulk stores; the other CTAs of the group leave at once
-            if (tile % GM_FWD_ZGROUP) return;
+            // one zeroed shared buffer re-sent through TMA bulk stores
             float4 *z4 = reinterpret_cast<float4 *>(smem);
             const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
             const int nz4 = (int)(A.acc_floats >> 2);
             for (int q = tid; q < nz4; q += kThreads) z4[q] = z;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
-            const int t1 = min(tile + GM_FWD_ZGROUP, (int)gridDim.y);
-            const int i1 = (t1 - 1) / A.ntj * TI, jl = ((t1 - 1) % A.ntj) * TJ;
-            // end of the last tile of the group: plane min(i1+TI, D), row band jl
-            const size_t end = min(TJ + jl, D) == D
-                                   ? (size_t)min(i1 + TI, D) * plane
-                                   : (size_t)i1 * plane + (size_t)(jl + TJ) * D;
-            float *slab = A.out + ((size_t)e * A.C + c) * D * plane;
-            const size_t begin = (size_t)i0 * plane + (size_t)j0 * D;
-            const size_t total = end - begin, per = (size_t)nz4 * 4;
+            const size_t per = (size_t)nz4 * 4;
             const size_t nst = (total + per - 1) / per;
             for (size_t q = tid; q < nst; q += kThreads) {
                 const size_t o = q * per;
@@ -194,8 +209,7 @@ __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         } else {
-            for (int p = 0; p < TIv; p++)
-                for (int q = tid; q < chunk; q += kThreads) __stcs(obase + p * plane + q, 0.f);
+            for (size_t q = tid; q < total; q += kThreads) __stcs(slab + begin + q, 0.f);
         }
         return;
     }
@@ -398,12 +412,16 @@ FwdConfig choose_config(int D) {
 }
 
 template <bool BIN, bool VEC, bool RESL>
-gm_status launch(const FwdArgs &A, const FwdConfig &cfg, int nex, cudaStream_t s) {
+gm_status launch(const FwdArgs &A, const FwdConfig &cfg, int nex, int njobs, cudaStream_t s) {
     auto kern = k_forward<BIN, VEC, RESL>;
     CUDA_TRY(gm_ensure_smem((const void *)kern, (int)cfg.smem));
-    const int ntiles = ((A.D + cfg.TI - 1) / cfg.TI) * A.ntj;
-    if (ntiles > 65535 || nex > 65535) return gm_fail(GM_ERR_INVALID, "too many examples or tiles");
-    dim3 grid(A.C, ntiles, nex);
+    if (A.jobs) {
+        if (njobs > 0) kern<<<njobs, kThreads, cfg.smem, s>>>(A);
+        LAUNCH_CHECK();
+        return GM_OK;
+    }
+    if (A.ntiles > 65535 || nex > 65535) return gm_fail(GM_ERR_INVALID, "too many examples or tiles");
+    dim3 grid(A.C, A.ntiles, nex);
     kern<<<grid, kThreads, cfg.smem, s>>>(A);
     LAUNCH_CHECK();
     return GM_OK;
@@ -436,10 +454,41 @@ gm_status forward_impl(const gm_params *p, const gm_batch *b, const Workspace &w
     A.rpw = cfg.rpw;
     A.bulk = (D % 4) == 0 && ((uintptr_t)out % 16) == 0;
     A.acc_floats = cfg.acc_floats;
+    A.ntiles = ((D + cfg.TI - 1) / cfg.TI) * A.ntj;
+    const bool jobs = b->fwd_jobs && b->fwd_jobs_npts == D && b->nfwd_jobs >= 0;
+    A.jobs = jobs ? reinterpret_cast<const int4 *>(b->fwd_jobs) : nullptr;
+    const int nj = jobs ? b->nfwd_jobs : 0;
     if (p->binary)
-        return b->vector_mode ? launch<true, true, false>(A, cfg, b->nexamples, s)
-                              : launch<true, false, false>(A, cfg, b->nexamples, s);
+        return b->vector_mode ? launch<true, true, false>(A, cfg, b->nexamples, nj, s)
+                              : launch<true, false, false>(A, cfg, b->nexamples, nj, s);
     // resolutions exactly representable in f32 (0.5, 0.25, 0.375 ...) drop the lo term
-    return A.resl != 0.0f ? launch<false, false, true>(A, cfg, b->nexamples, s)
-                          : launch<false, false, false>(A, cfg, b->nexamples, s);
+    return A.resl != 0.0f ? launch<false, false, true>(A, cfg, b->nexamples, nj, s)
+                          : launch<false, false, false>(A, cfg, b->nexamples, nj, s);
+}
+
+// Job table of a static grouping, in the dense launch's (example, tile,
+// channel) order minus the CTAs that would only exit: every tile of a channel
+// with items, and the first tile of each GM_FWD_ZGROUP group of a zero slab.
+int32_t forward_jobs_impl(const gm_params *p, int32_t nex, int32_t nch, const int32_t *co,
+                          int32_t *jobs, int32_t cap) {
+    const int D = p->npts;
+    const FwdConfig cfg = choose_config(D);
+    const int ntj = (D + cfg.TJ - 1) / cfg.TJ;
+    const int ntiles = ((D + cfg.TI - 1) / cfg.TI) * ntj;
+    long long n = 0;
+    for (int e = 0; e < nex; e++)
+        for (int t = 0; t < ntiles; t++)
+            for (int c = 0; c < nch; c++) {
+                const int cs = co[(size_t)e * (nch + 1) + c], ce = co[(size_t)e * (nch + 1) + c + 1];
+                if (cs == ce && t % GM_FWD_ZGROUP) continue;
+                if (jobs && n < cap) {
+                    int32_t *j = jobs + 4 * n;
+                    j[0] = e * nch + c;
+                    j[1] = t;
+                    j[2] = cs;
+                    j[3] = ce;
+                }
+                if (++n > 0x7fffffffLL) return -1;
+            }
+    return (int32_t)n;
 }

@@ -16,6 +16,7 @@ per-call arrays (origins, transforms) are uploaded separately.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -24,6 +25,8 @@ from . import _native
 from .errors import ConfigError
 
 _ALIGN = 256
+# GM_NO_JOBS=1: dense forward launch (A/B timing of the job table)
+_NO_JOBS = os.environ.get("GM_NO_JOBS", "") not in ("", "0")
 
 
 class _Layout:
@@ -295,6 +298,30 @@ class PackedBatch:
         if self._gm is not None:
             self._gm.xforms = (self._percall.data_ptr() + 8 * 3 * self.nexamples
                                if self._has_xforms else None)
+
+    def ensure_fwd_jobs(self, params) -> None:
+        """Forward job table of the static grouping for ``params.npts`` (built
+        once per grid size by the C ABI, uploaded once, cached)."""
+        npts = int(params.npts)
+        if _NO_JOBS or self._gm is None or getattr(self, "_jobs_npts", None) == npts or \
+                not self.nexamples or not self.nchannels:
+            return
+        off = self.offsets["chan_off"][0]
+        n = self.nexamples * (self.nchannels + 1)
+        co = np.ascontiguousarray(self.host.numpy()[off:off + 4 * n].view(np.int32))
+        lib = _native.lib()
+        cnt = lib.gm_forward_jobs(ctypes.byref(params), self.nexamples, self.nchannels,
+                                  co.ctypes.data, None, 0)
+        if cnt < 0:
+            return
+        jobs = np.zeros((max(cnt, 1), 4), np.int32)
+        lib.gm_forward_jobs(ctypes.byref(params), self.nexamples, self.nchannels,
+                            co.ctypes.data, jobs.ctypes.data, cnt)
+        self._jobs = torch.from_numpy(jobs).to(self.device)
+        self._jobs_npts = npts
+        self._gm.fwd_jobs = self._jobs.data_ptr()
+        self._gm.nfwd_jobs = int(cnt)
+        self._gm.fwd_jobs_npts = npts
 
     def gm_batch(self) -> _native.GmBatch:
         """The C-ABI batch descriptor (built once; pointers are stable)."""

@@ -275,6 +275,7 @@ class GridMaker:
         p = self._prepare(pb, centers, transforms, npts)
         if pb.nexamples and pb.nchannels:
             with torch.cuda.device(pb.device):
+                pb.ensure_fwd_jobs(p)
                 if events is not None:
                     events[0].record()
                 _native.check(_native.lib().gm_forward(

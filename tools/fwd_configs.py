@@ -20,6 +20,7 @@ for name in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["c2", "c5"]):
     out = torch.empty((pb.nexamples, pb.nchannels, D, D, D), device="cuda")
     xf = geom.draw_transform_array(pb.default_centers, 2.0, True, np.random.default_rng(0))
     p = gm._prepare(pb, None, xf, D)
+    pb.ensure_fwd_jobs(p)  # the job table, as forward_packed uses it
     st = stream_handle(pb.device)
     fn = lambda: lib.gm_forward(ctypes.byref(p), ctypes.byref(pb._gm), pb.workspace.data_ptr(),  # noqa: E731
                                 out.data_ptr(), st)
