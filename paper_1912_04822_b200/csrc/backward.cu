@@ -160,6 +160,9 @@ constexpr int kBwdWarps = GM_BWD_WARPS;
 #ifndef GM_BWD_F2F
 #define GM_BWD_F2F 1  // widen grid gradients with F2F (XU) instead of integer ops
 #endif
+#ifndef GM_BWDV_MINB
+#define GM_BWDV_MINB 16  // vector-mode backward: resident one-warp CTAs per SM
+#endif
 #ifndef GM_BWD_MINB
 #define GM_BWD_MINB 32
 #endif
@@ -178,6 +181,7 @@ struct __align__(8) RowEntry {
 
 struct WarpBwd {
     double dz[kTab], ez[kTab], dx[kTab], ex[kTab], dy[kTab], ey[kTab];
+    double wt[kMaxT];  // vector mode: the atom's type weights (broadcast reads)
     RowEntry rows[kRows];
     unsigned starts[kRows * kTab / 32 + kU];  // bit v: a row starts at flattened voxel v
 };
@@ -474,7 +478,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
 // channels the geometry is shared by all channels of the set: one walk, all
 // channel gradients per voxel, the coordinate term from sum_c w_c g_c.  With
 // type-indexed radii (or more channels) each channel walks its own box.
-__global__ void __launch_bounds__(kBwdWarps * 32) k_backward_vector(const BwdArgs P) {
+__global__ void __launch_bounds__(kBwdWarps * 32, GM_BWDV_MINB) k_backward_vector(const BwdArgs P) {
     __shared__ WarpBwd wsm[kBwdWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int a = blockIdx.x * kBwdWarps + warp;
@@ -499,12 +503,14 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_backward_vector(const BwdArg
         const double q0 = (2.0 * grm) / r;
         const double qa = P.eg * (q0 * q0);
         const double m4inv_r2 = -4.0 / (r * r);
-        double w[kMaxT], tg[kMaxT];
+        double tg[kMaxT];
 #pragma unroll
-        for (int c = 0; c < kMaxT; c++) {
-            w[c] = c < Tn ? (double)b.weights[row + c] : 0.0;
-            tg[c] = 0.0;
-        }
+        for (int c = 0; c < kMaxT; c++) tg[c] = 0.0;
+        // the weights live in shared memory (broadcast reads): registers go
+        // to the per-channel type-gradient accumulators
+        double *w = wsm[warp].wt;
+        if (lane < kMaxT) w[lane] = lane < Tn ? (double)b.weights[row + lane] : 0.0;
+        __syncwarp();
         if (set_radius(A, r, rmult, res, D)) {
             const double dzr = A.dzr, dzr2 = A.dzr2;
             flat_walk<false>(A, wsm[warp], gset, D, res, inv_res, lane, 1.0,
@@ -530,7 +536,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_backward_vector(const BwdArg
 #pragma unroll
                                  for (int c = 0; c < kMaxT; c++) {
                                      if (c < Tn) {
-                                         const double g = widen(gc[c]);
+                                         const double g = (double)gc[c];
                                          tg[c] = fma(g, dens, tg[c]);
                                          sw = fma(w[c], g, sw);
                                      }
