@@ -188,7 +188,7 @@ struct WarpBwd {
 
 // f(slot, d2, R, dz, ez, voxel_offset, g): every voxel of the box with
 // d2 < dzr2 (others get g = 0 / are skipped), g loaded by the walk when LOADG.
-template <bool LOADG, typename F>
+template <bool LOADG, int KU = kU, typename F>
 __device__ __forceinline__ void flat_walk(const Atom &A, WarpBwd &W, const float *gbase, int D,
                                           double res, float inv_res, int lane, double exy_scale,
                                           F &&f) {
@@ -221,7 +221,7 @@ __device__ __forceinline__ void flat_walk(const Atom &A, WarpBwd &W, const float
                     // ---- phase 1: row spans, compacted with a warp scan ----
                     int nrow = 0, total = 0;
                     const int nwords = (min(nrows_all - rb, kRows) * nk + 31) >> 5;
-                    for (int w = lane; w < nwords + kU; w += 32) W.starts[w] = 0u;
+                    for (int w = lane; w < nwords + KU; w += 32) W.starts[w] = 0u;
                     __syncwarp();
                     const int rend = min(nrows_all, rb + kRows);
                     for (int r0 = rb; r0 < rend; r0 += 32) {
@@ -266,23 +266,23 @@ __device__ __forceinline__ void flat_walk(const Atom &A, WarpBwd &W, const float
                         total += __shfl_sync(0xffffffffu, sc, 31);
                     }
                     __syncwarp();
-                    // ---- phase 2: kU windows of 32 voxels per step ----
+                    // ---- phase 2: KU windows of 32 voxels per step ----
                     // voxel v's row = (row starts <= v) - 1: one bitmap word per window
                     const unsigned le = 0xffffffffu >> (31 - lane);
                     int cur = -1;  // rows started before the next window, minus one
-                    for (int base = 0; base < total; base += 32 * kU) {
-                        int myrow[kU];
+                    for (int base = 0; base < total; base += 32 * KU) {
+                        int myrow[KU];
 #pragma unroll
-                        for (int u = 0; u < kU; u++) {
+                        for (int u = 0; u < KU; u++) {
                             const unsigned M = W.starts[(base >> 5) + u];
                             myrow[u] = cur + __popc(M & le);
                             cur += __popc(M);
                         }
-                        float g[kU];
-                        int kk[kU];
-                        int vo[kU];
+                        float g[KU];
+                        int kk[KU];
+                        int vo[KU];
 #pragma unroll
-                        for (int u = 0; u < kU; u++) {
+                        for (int u = 0; u < KU; u++) {
                             const int v = base + 32 * u + lane;
                             g[u] = 0.0f;
                             kk[u] = 0;
@@ -295,7 +295,7 @@ __device__ __forceinline__ void flat_walk(const Atom &A, WarpBwd &W, const float
                             }
                         }
 #pragma unroll
-                        for (int u = 0; u < kU; u++) {
+                        for (int u = 0; u < KU; u++) {
                             const int v = base + 32 * u + lane;
                             if (v < total) {
                                 const RowEntry &R = W.rows[myrow[u]];
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWDV_MINB) k_backward_vecto
         __syncwarp();
         if (set_radius(A, r, rmult, res, D)) {
             const double dzr = A.dzr, dzr2 = A.dzr2;
-            flat_walk<false>(A, wsm[warp], gset, D, res, inv_res, lane, 1.0,
+            flat_walk<false, 1>(A, wsm[warp], gset, D, res, inv_res, lane, 1.0,
                              [&](int, double d2, const RowEntry &R, double dz, double ez,
                                  size_t voff, float) {
                                  if (d2 >= dzr2) return;
@@ -530,8 +530,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWDV_MINB) k_backward_vecto
                                  const float *gv = gset + voff;
                                  float gc[kMaxT];
 #pragma unroll
-                                 for (int c = 0; c < kMaxT; c++)
-                                     gc[c] = c < Tn ? __ldg(gv + c * D3) : 0.0f;
+                                 for (int c = 0; c < kMaxT; c++, gv += D3)
+                                     gc[c] = c < Tn ? __ldg(gv) : 0.0f;
                                  double sw = 0.0;
 #pragma unroll
                                  for (int c = 0; c < kMaxT; c++) {
