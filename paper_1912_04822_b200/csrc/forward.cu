@@ -25,6 +25,8 @@
 // Consecutive CTAs are the channels of one tile, so scatter work and the
 // stores of empty channels interleave finely (HBM keeps writing while SMs
 // compute).
+#include <vector>
+
 #include "common.cuh"
 
 namespace {
@@ -37,6 +39,16 @@ namespace {
 #endif
 #ifndef GM_FWD_ZGROUP
 #define GM_FWD_ZGROUP 8  // tiles of a zero slab written by one CTA
+#endif
+#ifndef GM_FWD_LPT
+#define GM_FWD_LPT 2  // job table: 0 dense order, 1 heaviest first, 2 heavy/light alternating
+#endif
+#ifndef GM_FWD_LPT_GROUP
+#define GM_FWD_LPT_GROUP 0  // examples per reordering group (0: the whole batch)
+#endif
+#ifndef GM_FWD_LPT_MAXD
+#define GM_FWD_LPT_MAXD 64  // reorder only up to this grid size (measured: 48^3 gains
+                            // 14%, 96^3 loses 8% -- its store-bound tiles want the dense order)
 #endif
 #ifndef GM_FWD_BUDGET_KB
 #define GM_FWD_BUDGET_KB 10
@@ -466,29 +478,76 @@ gm_status forward_impl(const gm_params *p, const gm_batch *b, const Workspace &w
                           : launch<false, false, false>(A, cfg, b->nexamples, nj, s);
 }
 
-// Job table of a static grouping, in the dense launch's (example, tile,
-// channel) order minus the CTAs that would only exit: every tile of a channel
-// with items, and the first tile of each GM_FWD_ZGROUP group of a zero slab.
+// Job table of a static grouping: every tile of a channel with items, and the
+// first tile of each GM_FWD_ZGROUP group of a zero slab -- none of the dense
+// launch's CTAs that would only exit.  On small grids the scatter jobs are
+// reordered by their channel's item count, alternating the heaviest and the
+// lightest remaining job, so every wave mixes long scatter tiles with short
+// store-bound ones and no many-item tile is left to close the launch; the zero
+// groups are spread evenly between them so HBM keeps writing while SMs scatter.
 int32_t forward_jobs_impl(const gm_params *p, int32_t nex, int32_t nch, const int32_t *co,
                           int32_t *jobs, int32_t cap) {
     const int D = p->npts;
     const FwdConfig cfg = choose_config(D);
     const int ntj = (D + cfg.TJ - 1) / cfg.TJ;
     const int ntiles = ((D + cfg.TI - 1) / cfg.TI) * ntj;
-    long long n = 0;
+    struct Job { int32_t slab, tile, cs, ce; };
+    std::vector<Job> work, zero;
     for (int e = 0; e < nex; e++)
         for (int t = 0; t < ntiles; t++)
             for (int c = 0; c < nch; c++) {
                 const int cs = co[(size_t)e * (nch + 1) + c], ce = co[(size_t)e * (nch + 1) + c + 1];
-                if (cs == ce && t % GM_FWD_ZGROUP) continue;
-                if (jobs && n < cap) {
-                    int32_t *j = jobs + 4 * n;
-                    j[0] = e * nch + c;
-                    j[1] = t;
-                    j[2] = cs;
-                    j[3] = ce;
+                if (cs == ce) {
+                    if (t % GM_FWD_ZGROUP == 0) zero.push_back({e * nch + c, t, cs, ce});
+                } else {
+                    work.push_back({e * nch + c, t, cs, ce});
                 }
-                if (++n > 0x7fffffffLL) return -1;
             }
+    const long long n = (long long)work.size() + (long long)zero.size();
+    if (n > 0x7fffffffLL) return -1;
+    if (jobs && D <= GM_FWD_LPT_MAXD) {
+#if GM_FWD_LPT
+        // heaviest first within groups of GM_FWD_LPT_GROUP examples (0: globally)
+        const int G = GM_FWD_LPT_GROUP > 0 ? GM_FWD_LPT_GROUP : std::max(nex, 1);
+        std::stable_sort(work.begin(), work.end(), [=](const Job &a, const Job &b) {
+            const int ga = a.slab / nch / G, gb = b.slab / nch / G;
+            if (ga != gb) return ga < gb;
+            return a.ce - a.cs > b.ce - b.cs;
+        });
+#if GM_FWD_LPT == 2
+        // alternate the heavy and light ends of each group: every wave mixes
+        // scatter-bound and store-bound tiles
+        std::vector<Job> mixed;
+        mixed.reserve(work.size());
+        for (size_t g0 = 0; g0 < work.size();) {
+            size_t g1 = g0;
+            const int grp = work[g0].slab / nch / G;
+            while (g1 < work.size() && work[g1].slab / nch / G == grp) g1++;
+            size_t lo = g0, hi = g1;
+            bool heavy = true;
+            while (lo < hi) {
+                mixed.push_back(heavy ? work[lo++] : work[--hi]);
+                heavy = !heavy;
+            }
+            g0 = g1;
+        }
+        work.swap(mixed);
+#endif
+#endif
+    }
+    if (jobs) {
+        size_t wi = 0, zi = 0;
+        for (long long k = 0; k < n && k < cap; k++) {
+            // zero job k' goes where the running share of zero jobs falls behind
+            const bool z = zi < zero.size() &&
+                           (wi >= work.size() || (zi + 1) * (double)n <= (k + 1) * (double)zero.size() + 1e-9);
+            const Job &j = z ? zero[zi++] : work[wi++];
+            int32_t *o = jobs + 4 * k;
+            o[0] = j.slab;
+            o[1] = j.tile;
+            o[2] = j.cs;
+            o[3] = j.ce;
+        }
+    }
     return (int32_t)n;
 }
