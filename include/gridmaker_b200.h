@@ -104,6 +104,10 @@ typedef struct {
     const int32_t *fwd_jobs;
     int32_t nfwd_jobs;
     int32_t fwd_jobs_npts;
+    /* optional (natoms) index-mode backward launch slot of each atom (a
+     * permutation), or NULL = atom order.  Cost-balanced orders shorten the
+     * backward's tail; results do not depend on it. */
+    const int32_t *bwd_slot;
 } gm_batch;
 
 /* Device scratch needed by gm_prepare / gm_forward / gm_backward. */

@@ -336,15 +336,16 @@ struct WarpIdx {
 __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(const BwdArgs P) {
     __shared__ WarpIdx wsm[kBwdWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int a = blockIdx.x * kBwdWarps + warp;
-    if (a >= P.b.natoms) return;
+    const int rec = blockIdx.x * kBwdWarps + warp;  // record slot (launch order)
+    if (rec >= P.b.natoms) return;
     WarpIdx &W = wsm[warp];
     const int D = P.p.npts;
     const double res = P.p.resolution;
     const float inv_res = (float)(1.0 / res);
     // the prepare pass's record: position relative to the origin, constants,
     // and the forward item's box (_kernels.py:225-227) -- one load level
-    const BwdAtom B = P.batoms[a];
+    const BwdAtom B = P.batoms[rec];
+    const int a = B.atom;
     const int i0 = box_lo(B.ibox), i1 = box_hi(B.ibox), j0 = box_lo(B.jbox),
               j1 = box_hi(B.jbox), k0 = box_lo(B.kbox), k1 = box_hi(B.kbox);
     const double dzr = B.dzr, dzr2 = B.dzr2, d02 = B.d02, qa2 = B.qa2;

@@ -65,7 +65,8 @@ struct __align__(16) BwdAtom {
     double lx, ly, lz;       // transformed position minus the example's origin
     double dzr, dzr2, d02;   // cutoff rmult*r and its square, (grm r)^2
     double qa2, m4inv_r2;    // 2 qa (_kernels.py:224 tail slope), -4 / r^2
-    double m2inv_r2, pad;    // -2 / r^2 (per-axis Gaussian tables)
+    double m2inv_r2;         // -2 / r^2 (per-axis Gaussian tables)
+    int atom, pad;           // packed atom index (records may be permuted: gm_batch.bwd_slot)
     int slab;                // e * nchannels + channel: the atom's grid_grad block
     int ibox, jbox, kbox;    // voxel box (lo | hi << 16); ibox lo > hi if it misses
 };

@@ -160,12 +160,13 @@ __device__ __forceinline__ void store_bwd_atom(const PrepArgs &A, int a, int e, 
     w.qa2 = 2.0 * (A.eg * (q0 * q0));
     w.m4inv_r2 = -4.0 / (r * r);
     w.m2inv_r2 = 0.5 * w.m4inv_r2;
-    w.pad = 0.0;
+    w.atom = a;
+    w.pad = 0;
     w.slab = e * A.b.nchannels + ch;
     w.ibox = f.ibox;
     w.jbox = f.jbox;
     w.kbox = f.kbox;
-    A.ws.batoms[a] = w;
+    A.ws.batoms[A.b.bwd_slot ? A.b.bwd_slot[a] : a] = w;
 }
 
 __device__ __forceinline__ int make_item(const PrepArgs &A, int it, int a, const double x3[3],
