@@ -285,3 +285,41 @@ def test_example_too_big_for_smem_staging(binary, rng):
         np.testing.assert_array_equal(grid, ref)
     else:
         assert_close(grid, ref, what="global-staged forward")
+
+
+def test_launch_orders_do_not_change_results(monkeypatch):
+    """The forward job table (tile order, skipped zero CTAs) and the backward's
+    cost-ordered launch are scheduling only: results are bitwise identical to
+    the dense launch in atom order."""
+    from paper_1912_04822_b200 import GridMaker, packing, synthetic
+
+    exs = synthetic.batch(6, seed=31)
+    gm = GridMaker()
+    g1, xf = gm.forward_batch(exs, random_rotation=True, random_translation=2.0,
+                              rng=np.random.default_rng(4), return_transforms=True)
+    b1 = gm.backward_batch(exs, g1, transforms=xf)
+    monkeypatch.setattr(packing, "_NO_JOBS", True)
+    monkeypatch.setattr(packing, "_BWD_ORDER", "none")
+    g2 = gm.forward_batch(exs, random_rotation=True, random_translation=2.0,
+                          rng=np.random.default_rng(4))
+    b2 = gm.backward_batch(exs, g1, transforms=xf)
+    np.testing.assert_array_equal(g1, g2)
+    for e1, e2 in zip(b1, b2):
+        for (c1, _), (c2, _) in zip(e1, e2):
+            np.testing.assert_array_equal(c1, c2)
+
+
+def test_job_table_with_dynamic_grouping_path():
+    """More examples than the inline prepare takes (GM_INLINE_MAX_EXAMPLES):
+    the per-example grouping pass runs and the forward re-reads its ranges."""
+    from paper_1912_04822_b200 import GridMaker, synthetic
+
+    rng = np.random.default_rng(32)
+    exs = [synthetic.complex_example(rng, n_receptor=40, n_ligand=6) for _ in range(205)]
+    gm = gm_of({"dimension": 11.5})
+    grid = gm.forward_batch(exs, random_rotation=True, random_translation=2.0,
+                            rng=np.random.default_rng(6))
+    go = oracle.GridOracle(dimension=11.5)
+    ref = go.forward_batch(exs, random_rotation=True, random_translation=2.0,
+                           rng=np.random.default_rng(6))
+    assert_close(grid, ref, what="205-example batch")
