@@ -50,6 +50,9 @@ namespace {
 #define GM_FWD_LPT_MAXD 64  // reorder only up to this grid size (measured: 48^3 gains
                             // 14%, 96^3 loses 8% -- its store-bound tiles want the dense order)
 #endif
+#ifndef GM_FWD_ZPLACE
+#define GM_FWD_ZPLACE 0  // zero groups in the job table: 0 spread evenly, 1 first, 2 last
+#endif
 #ifndef GM_FWD_BUDGET_KB
 #define GM_FWD_BUDGET_KB 10
 #endif
@@ -539,8 +542,14 @@ int32_t forward_jobs_impl(const gm_params *p, int32_t nex, int32_t nch, const in
         size_t wi = 0, zi = 0;
         for (long long k = 0; k < n && k < cap; k++) {
             // zero job k' goes where the running share of zero jobs falls behind
+#if GM_FWD_ZPLACE == 1  // zero groups first
+            const bool z = zi < zero.size();
+#elif GM_FWD_ZPLACE == 2  // zero groups last
+            const bool z = wi >= work.size();
+#else
             const bool z = zi < zero.size() &&
                            (wi >= work.size() || (zi + 1) * (double)n <= (k + 1) * (double)zero.size() + 1e-9);
+#endif
             const Job &j = z ? zero[zi++] : work[wi++];
             int32_t *o = jobs + 4 * k;
             o[0] = j.slab;
