@@ -108,6 +108,11 @@ typedef struct {
      * permutation), or NULL = atom order.  Cost-balanced orders shorten the
      * backward's tail; results do not depend on it. */
     const int32_t *bwd_slot;
+    /* optional (nitems) index-mode slot records of the static grouping, 48 B each
+     * in item_perm order: f32 x, y, z; int32 atom, absolute channel, example,
+     * single-atom-set flag, backward slot; f64 radius * scale; 8 B pad.
+     * Lets gm_prepare_inline start from one coalesced load per item. */
+    const void *slot_rec;
 } gm_batch;
 
 /* Device scratch needed by gm_prepare / gm_forward / gm_backward. */

@@ -183,6 +183,22 @@ __device__ __forceinline__ int make_item(const PrepArgs &A, int it, int a, const
 // the grid stay in their channel's range with an empty box (ibox lo > hi), so
 // the forward's cull and the backward's box test skip them.
 // ---------------------------------------------------------------------------
+// Index mode, static grouping: everything the prepare pass needs about the
+// item in slot t, gathered once at pack time (gm_batch.slot_rec), so the
+// pass starts from ONE coalesced load instead of three dependent ones
+// (item_perm -> atom arrays -> set arrays).
+struct __align__(16) SlotRec {
+    float x, y, z;    // input-frame coordinates (coords32)
+    int atom;         // packed atom index
+    int ch;           // absolute output channel (set_choff + type)
+    int ex;           // example
+    int single;       // 1: the atom's set has one atom (numpy's (1,3)@(3,3) FMA order)
+    int bslot;        // backward launch slot (gm_batch.bwd_slot, else atom)
+    double r;         // radius * radius_scale
+    double pad;
+};
+static_assert(sizeof(SlotRec) == 48, "SlotRec must be 48 bytes");
+
 template <int CAP>
 struct CallArgs {
     int nex, has_xf;
@@ -204,7 +220,72 @@ __global__ void __launch_bounds__(GM_PREP_THREADS) k_prepare_static(const PrepAr
         transform_atom_x(A, t, s, K.has_xf ? K.v + 3 * nex + 15 * e : nullptr, x);
         store_pos(A, t, x);
     }
-    if (t < b.nitems) {
+    if (!vector && b.slot_rec && t < b.nitems) {
+        const SlotRec R = reinterpret_cast<const SlotRec *>(b.slot_rec)[t];
+        const gm_params &p = A.p;
+        const int D = p.npts, e = R.ex, a = R.atom;
+        const double *X = K.has_xf ? K.v + 3 * nex + 15 * e : nullptr;
+        const double *O = K.v + 3 * e;
+        double x[3] = {(double)R.x, (double)R.y, (double)R.z};
+        if (X) {  // geom.py:105 in numpy's FMA order
+            const double d[3] = {__dsub_rn(x[0], X[9]), __dsub_rn(x[1], X[10]),
+                                 __dsub_rn(x[2], X[11])};
+#pragma unroll
+            for (int j = 0; j < 3; j++)
+                x[j] = __dadd_rn(__dadd_rn(dot3(d, X + 3 * j, R.single ? p.matmul_order_1
+                                                                            : p.matmul_order_n),
+                                           X[9 + j]), X[12 + j]);
+        }
+        store_pos(A, a, x);
+        const double res = p.resolution, grm = p.gaussian_radius_multiple, rmult = p.radius_multiple;
+        const double r = R.r;
+        const double cut = p.binary ? r : __dmul_rn(r, rmult);
+        int i0, i1, j0, j1, k0, k1;
+        axis_bounds(x[0], cut, O[0], res, D, i0, i1);
+        axis_bounds(x[1], cut, O[1], res, D, j0, j1);
+        axis_bounds(x[2], cut, O[2], res, D, k0, k1);
+        const bool valid = i0 <= i1 && j0 <= j1 && k0 <= k1;
+        FwdItem f;
+        split_hilo((double)i0 * res - (x[0] - O[0]), f.cxh, f.cxl);
+        split_hilo((double)j0 * res - (x[1] - O[1]), f.cyh, f.cyl);
+        split_hilo((double)k0 * res - (x[2] - O[2]), f.czh, f.czl);
+        const double r2 = r * r;
+        f.cexp = (float)((-2.0 * CUDART_L2E) / r2);
+        const double gr = grm * r;
+        f.d02 = (float)(gr * gr);
+        f.dzr = (float)cut;
+        const double q0 = (2.0 * grm) / r;
+        const double qa = A.eg * (q0 * q0);
+        f.qa = (float)qa;
+        f.w = 1.0f;
+        f.ch = R.ch;
+        f.ibox = valid ? (i0 | (i1 << 16)) : 0x7fff;  // empty: the forward skips it
+        f.jbox = j0 | (j1 << 16);
+        f.kbox = k0 | (k1 << 16);
+        f.atom = a;
+        A.ws.sorted[t] = f;
+        A.ws.sbox[t] = make_int2(f.ibox, f.jbox);
+        if (p.binary) A.ws.bsorted[t] = BinItem{x[0], x[1], x[2], __dmul_rn(r, r)};
+        // the backward's record (_kernels.py:224-251 constants, same box)
+        BwdAtom w;
+        w.lx = x[0] - O[0];
+        w.ly = x[1] - O[1];
+        w.lz = x[2] - O[2];
+        w.dzr = rmult * r;
+        w.dzr2 = w.dzr * w.dzr;
+        const double d0 = grm * r;
+        w.d02 = d0 * d0;
+        w.qa2 = 2.0 * qa;
+        w.m4inv_r2 = -4.0 / (r * r);
+        w.m2inv_r2 = 0.5 * w.m4inv_r2;
+        w.atom = a;
+        w.pad = 0;
+        w.slab = e * b.nchannels + R.ch;
+        w.ibox = f.ibox;
+        w.jbox = f.jbox;
+        w.kbox = f.kbox;
+        A.ws.batoms[R.bslot] = w;
+    } else if (t < b.nitems) {
         const int it = b.item_perm[t];
         const int a = vector ? b.item_atom[it] : it;
         const int s = b.atom_set[a];
@@ -219,8 +300,6 @@ __global__ void __launch_bounds__(GM_PREP_THREADS) k_prepare_static(const PrepAr
         A.ws.sorted[t] = f;
         A.ws.sbox[t] = make_int2(f.ibox, f.jbox);
         if (A.p.binary) A.ws.bsorted[t] = bi;
-        // packed order: the index-mode backward reads its boxes
-        *reinterpret_cast<int4 *>(&A.ws.items[it].ibox) = make_int4(f.ibox, f.jbox, f.kbox, f.atom);
     }
 }
 

@@ -109,6 +109,7 @@ class PackedBatch:
             L.add("atom_type", atom_type)
             slot = _bwd_slots(coords, set_example[atom_set] if self.natoms else atom_set,
                               example_sets)
+            self._bwd_slot_host = slot
             if slot is not None:
                 L.add("bwd_slot", slot)
             for s in range(self.nsets):
@@ -192,6 +193,19 @@ class PackedBatch:
         chan_off = np.searchsorted(key[perm], bounds.reshape(-1), side="left").astype(np.int32)
         L.add("item_perm", perm)
         L.add("chan_off", chan_off)
+        if not self.vector_mode and self.nitems:
+            # index mode: per-slot records (gm_batch.slot_rec), item_perm order
+            rec = np.zeros(self.nitems, _SLOT_DTYPE)
+            a = perm.astype(np.int64)
+            rec["x"], rec["y"], rec["z"] = coords[a, 0], coords[a, 1], coords[a, 2]
+            rec["atom"] = a
+            rec["ch"] = chan[a]
+            rec["ex"] = set_example[atom_set[a]]
+            rec["single"] = (counts[atom_set[a]] == 1).astype(np.int32)
+            bs = self._bwd_slot_host
+            rec["bslot"] = bs[a] if bs is not None else a
+            rec["r"] = radius[a]
+            L.add("slot_rec", rec.view(np.uint8))
         self.offsets = L.offsets
 
         # one pinned staging buffer -> one device buffer
@@ -342,7 +356,7 @@ class PackedBatch:
                          "set_end", "set_example", "set_choff", "set_t", "set_wstart", "weights",
                          "type_radius", "set_trstart", "item_atom", "item_channel",
                          "item_weight", "item_radius", "ex_item_start", "ex_item_end",
-                         "item_perm", "chan_off", "bwd_slot"):
+                         "item_perm", "chan_off", "bwd_slot", "slot_rec"):
                 setattr(b, name, self.ptr(name))
             base = self._percall.data_ptr()
             b.origins = base
@@ -350,6 +364,12 @@ class PackedBatch:
             self._gm = b
         return self._gm
 
+
+# gm_batch.slot_rec record (include/gridmaker_b200.h)
+_SLOT_DTYPE = np.dtype([("x", "<f4"), ("y", "<f4"), ("z", "<f4"), ("atom", "<i4"), ("ch", "<i4"),
+                        ("ex", "<i4"), ("single", "<i4"), ("bslot", "<i4"), ("r", "<f8"),
+                        ("pad", "<f8")])
+assert _SLOT_DTYPE.itemsize == 48
 
 # GM_BWD_ORDER: backward launch order of the atoms -- "lpt" (default: heaviest
 # first; measured best, C2 100 -> 94.5 us), "alt" (heavy / light alternating)
