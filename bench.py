@@ -73,7 +73,7 @@ while True:
               pynvml.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)
     except Exception:
         break
-    time.sleep(0.002)
+    time.sleep(0.0005)
 """
 
 
@@ -321,7 +321,6 @@ def main():
         step()
     t_end.record(stream)
     barrier()
-    clk = clocks.stop()
     launches = _native.launch_count()
     ms = t_start.elapsed_time(t_end) / args.steps
     # kernel durations for the roofline: a second, instrumented pass of the
@@ -333,6 +332,9 @@ def main():
     for k in range(args.steps):
         step(fevs[k], bevs[k])
     barrier()
+    # clocks: sampled from the start of the headline pass to the end of the
+    # instrumented one (short runs would otherwise catch no sample)
+    clk = clocks.stop()
     fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in fevs)
     bwd_ms = statistics.mean(a.elapsed_time(b) for a, b in bevs)
     if ws > 1:
