@@ -475,6 +475,79 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
     store_coord(P, a, lane, gx, gy, gz);
 }
 
+// Vector types with per-atom radii: one geometry walk, every channel of the
+// set per voxel (type gradients, _kernels.py:296-313) and the coordinate
+// term from sum_c w_c g_c.  NT > 0: compile-time channel count (no
+// predicates, 32-bit channel offsets); NT = 0: up to kMaxT, predicated.
+template <int NT>
+__device__ __forceinline__ void vector_shared_walk(const BwdArgs &P, WarpBwd &W, Atom &A, int a,
+                                                   int row, int Tn, const float *gset, int D,
+                                                   double res, float inv_res, int lane,
+                                                   double &gx, double &gy, double &gz) {
+    constexpr int NC = NT > 0 ? NT : kMaxT;
+    const gm_batch &b = P.b;
+    const double grm = P.p.gaussian_radius_multiple, rmult = P.p.radius_multiple;
+    const double r = b.atom_radius[a];
+    const double gr = grm * r, d02 = gr * gr;
+    const double q0 = (2.0 * grm) / r;
+    const double qa = P.eg * (q0 * q0);
+    const double m4inv_r2 = -4.0 / (r * r);
+    const unsigned D3 = (unsigned)D * D * D;
+    double tg[NC];
+#pragma unroll
+    for (int c = 0; c < NC; c++) tg[c] = 0.0;
+    // the weights live in shared memory (broadcast reads): registers go to
+    // the per-channel type-gradient accumulators
+    double *w = W.wt;
+    if (lane < kMaxT) w[lane] = lane < Tn ? (double)b.weights[row + lane] : 0.0;
+    __syncwarp();
+    if (set_radius(A, r, rmult, res, D)) {
+        const double dzr = A.dzr, dzr2 = A.dzr2;
+        flat_walk<false, 1>(A, W, gset, D, res, inv_res, lane, 1.0,
+                            [&](int, double d2, const RowEntry &R, double dz, double ez,
+                                size_t voff, float) {
+                                if (d2 >= dzr2) return;
+                                double dens, sod;  // density, slope / d
+                                if (d2 <= d02) {
+                                    dens = R.exy * ez;
+                                    sod = dens * m4inv_r2;
+                                } else {
+                                    const double rd = rsqrt_d(d2);
+                                    const double t = fma(d2, rd, -dzr);
+                                    dens = (qa * t) * t;
+                                    sod = (2.0 * qa) * t * rd;
+                                }
+                                float gc[NC];
+                                unsigned off = (unsigned)voff;
+#pragma unroll
+                                for (int c = 0; c < NC; c++, off += D3)
+                                    gc[c] = (NT > 0 || c < Tn) ? __ldg(gset + off) : 0.0f;
+                                double sw = 0.0;
+#pragma unroll
+                                for (int c = 0; c < NC; c++) {
+                                    if (NT > 0 || c < Tn) {
+                                        const double g = (double)gc[c];
+                                        tg[c] = fma(g, dens, tg[c]);
+                                        sw = fma(w[c], g, sw);
+                                    }
+                                }
+                                if (d2 > 0.0) {
+                                    const double sc = sw * sod;
+                                    gx = fma(sc, R.dx, gx);
+                                    gy = fma(sc, R.dy, gy);
+                                    gz = fma(sc, dz, gz);
+                                }
+                            });
+    }
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+        if (NT > 0 || c < Tn) {
+            const double v = warp_sum(tg[c]);
+            if (lane == 0 && P.type_grad) P.type_grad[row + c] = (float)v;
+        }
+    }
+}
+
 // Vector types (_kernels.py:258-314).  With per-atom radii and <= kMaxT
 // channels the geometry is shared by all channels of the set: one walk, all
 // channel gradients per voxel, the coordinate term from sum_c w_c g_c.  With
@@ -499,64 +572,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWDV_MINB) k_backward_vecto
     double gx = 0.0, gy = 0.0, gz = 0.0;
 
     if (!P.p.radius_type_indexed && Tn <= kMaxT) {
-        const double r = b.atom_radius[a];
-        const double gr = grm * r, d02 = gr * gr;
-        const double q0 = (2.0 * grm) / r;
-        const double qa = P.eg * (q0 * q0);
-        const double m4inv_r2 = -4.0 / (r * r);
-        double tg[kMaxT];
-#pragma unroll
-        for (int c = 0; c < kMaxT; c++) tg[c] = 0.0;
-        // the weights live in shared memory (broadcast reads): registers go
-        // to the per-channel type-gradient accumulators
-        double *w = wsm[warp].wt;
-        if (lane < kMaxT) w[lane] = lane < Tn ? (double)b.weights[row + lane] : 0.0;
-        __syncwarp();
-        if (set_radius(A, r, rmult, res, D)) {
-            const double dzr = A.dzr, dzr2 = A.dzr2;
-            flat_walk<false, 1>(A, wsm[warp], gset, D, res, inv_res, lane, 1.0,
-                             [&](int, double d2, const RowEntry &R, double dz, double ez,
-                                 size_t voff, float) {
-                                 if (d2 >= dzr2) return;
-                                 double dens, sod;  // density, slope / d
-                                 if (d2 <= d02) {
-                                     dens = R.exy * ez;
-                                     sod = dens * m4inv_r2;
-                                 } else {
-                                     const double rd = rsqrt_d(d2);
-                                     const double t = fma(d2, rd, -dzr);
-                                     dens = (qa * t) * t;
-                                     sod = (2.0 * qa) * t * rd;
-                                 }
-                                 const float *gv = gset + voff;
-                                 float gc[kMaxT];
-#pragma unroll
-                                 for (int c = 0; c < kMaxT; c++, gv += D3)
-                                     gc[c] = c < Tn ? __ldg(gv) : 0.0f;
-                                 double sw = 0.0;
-#pragma unroll
-                                 for (int c = 0; c < kMaxT; c++) {
-                                     if (c < Tn) {
-                                         const double g = (double)gc[c];
-                                         tg[c] = fma(g, dens, tg[c]);
-                                         sw = fma(w[c], g, sw);
-                                     }
-                                 }
-                                 if (d2 > 0.0) {
-                                     const double sc = sw * sod;
-                                     gx = fma(sc, R.dx, gx);
-                                     gy = fma(sc, R.dy, gy);
-                                     gz = fma(sc, dz, gz);
-                                 }
-                             });
-        }
-#pragma unroll
-        for (int c = 0; c < kMaxT; c++) {
-            if (c < Tn) {
-                const double v = warp_sum(tg[c]);
-                if (lane == 0 && P.type_grad) P.type_grad[row + c] = (float)v;
-            }
-        }
+        // channel loops fully unrolled without predicates for the common
+        // 14-type table, predicated up to kMaxT otherwise
+        if (Tn == 14)
+            vector_shared_walk<14>(P, wsm[warp], A, a, row, Tn, gset, D, res, inv_res, lane, gx, gy, gz);
+        else
+            vector_shared_walk<0>(P, wsm[warp], A, a, row, Tn, gset, D, res, inv_res, lane, gx, gy, gz);
     } else {
         for (int c = 0; c < Tn; c++) {
             const double r = P.p.radius_type_indexed ? b.type_radius[b.set_trstart[s] + c]
