@@ -97,6 +97,7 @@ class ClockSampler:
                 idx = int(vis.split(",")[self.index])
             except ValueError:
                 idx = self.index
+        self.nvml_index = idx
         try:
             self.proc = subprocess.Popen([sys.executable, "-c", _CLOCK_PROBE, str(idx)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
@@ -116,6 +117,8 @@ class ClockSampler:
             self.proc.kill()
             out, _ = self.proc.communicate()
         sm, reasons = [], set()
+        if os.environ.get("GM_CLOCK_DEBUG"):
+            print("clock probe output:", repr(out[:400]), file=sys.stderr)
         for ln in out.splitlines():
             parts = ln.split()
             if len(parts) != 2:
@@ -129,7 +132,18 @@ class ClockSampler:
                 if bits & b:
                     reasons.add(name)
         if not sm:
-            return None
+            # a very short timed region can end before the probe's first
+            # sample: read the clocks once right after it instead
+            try:
+                import pynvml
+
+                pynvml.nvmlInit()
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.nvml_index)
+                sm = [float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))]
+                bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                reasons = {n for b, n in self.REASONS.items() if bits & b}
+            except Exception:
+                return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
