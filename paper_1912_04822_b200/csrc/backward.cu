@@ -33,6 +33,7 @@ struct BwdArgs {
     float *type_grad;
     const FwdItem *items;  // index mode: item a == atom a; its box (cut rmult*r) is reused
     const BwdAtom *batoms; // index mode: per-atom records of the prepare pass
+    const int32_t *atom_order; // vector mode: atom of each launch slot (bwd_slot inverse)
     double eg;             // exp(-2 grm^2), a batch constant (_kernels.py:224)
 };
 
@@ -580,9 +581,11 @@ __device__ __forceinline__ void vector_shared_walk(const BwdArgs &P, WarpBwd &W,
 __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWDV_MINB) k_backward_vector(const BwdArgs P) {
     __shared__ WarpBwd wsm[kBwdWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int a = blockIdx.x * kBwdWarps + warp;
+    const int slot = blockIdx.x * kBwdWarps + warp;
     const gm_batch &b = P.b;
-    if (a >= b.natoms) return;
+    if (slot >= b.natoms) return;
+    // heaviest atoms first when the batch carries a launch order (bwd_slot)
+    const int a = b.bwd_slot ? P.atom_order[slot] : slot;
     const int D = P.p.npts;
     const double res = P.p.resolution, grm = P.p.gaussian_radius_multiple,
                  rmult = P.p.radius_multiple;
@@ -660,6 +663,7 @@ gm_status backward_impl(const gm_params *p, const gm_batch *b, const Workspace &
     P.type_grad = type_grad;
     P.items = ws.items;
     P.batoms = ws.batoms;
+    P.atom_order = ws.atom_order;
     P.eg = exp((-2.0 * p->gaussian_radius_multiple) * p->gaussian_radius_multiple);
     if (b->vector_mode)
         k_backward_vector<<<(b->natoms + kBwdWarps - 1) / kBwdWarps, kBwdWarps * 32, 0, s>>>(P);

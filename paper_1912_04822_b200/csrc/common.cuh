@@ -88,6 +88,7 @@ struct Workspace {
     int2 *sbox;          // nitems: {ibox, jbox} of sorted items (forward culling)
     int32_t *chan_off;   // nexamples * (nchannels + 1): ranges into sorted
     BwdAtom *batoms;     // natoms (index mode): backward records
+    int32_t *atom_order; // natoms (vector mode with gm_batch.bwd_slot): atom of each launch slot
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -113,6 +114,7 @@ inline size_t carve_workspace(void *base, int32_t natoms, int32_t nitems, int32_
     ws->sbox = (int2 *)take(sizeof(int2) * ni);
     ws->chan_off = (int32_t *)take(sizeof(int32_t) * (size_t)std::max(nex, 1) * (nch + 1));
     ws->batoms = (BwdAtom *)take(sizeof(BwdAtom) * na);
+    ws->atom_order = (int32_t *)take(sizeof(int32_t) * na);
     return off + 256;
 }
 

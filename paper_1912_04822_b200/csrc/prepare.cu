@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(256) k_prepare_atoms(const PrepArgs A) {
         double x[3];
         transform_atom(A, a, x);
         store_pos(A, a, x);
+        if (A.b.vector_mode && A.b.bwd_slot) A.ws.atom_order[A.b.bwd_slot[a]] = a;
     }
 }
 
@@ -219,6 +220,7 @@ __global__ void __launch_bounds__(GM_PREP_THREADS) k_prepare_static(const PrepAr
         double x[3];
         transform_atom_x(A, t, s, K.has_xf ? K.v + 3 * nex + 15 * e : nullptr, x);
         store_pos(A, t, x);
+        if (b.bwd_slot) A.ws.atom_order[b.bwd_slot[t]] = t;  // vector backward launch order
     }
     if (!vector && b.slot_rec && t < b.nitems) {
         const SlotRec R = reinterpret_cast<const SlotRec *>(b.slot_rec)[t];
@@ -365,6 +367,7 @@ __global__ void __launch_bounds__(1024) k_prepare_example(const PrepArgs A) {
             double x[3];
             transform_atom(A, a, x);
             store_pos(A, a, x);
+            if (b.bwd_slot) A.ws.atom_order[b.bwd_slot[a]] = a;
         }
     }
     for (int q = threadIdx.x; q < n; q += blockDim.x) {
