@@ -113,6 +113,12 @@ typedef struct {
      * single-atom-set flag, backward slot; f64 radius * scale; 8 B pad.
      * Lets gm_prepare_inline start from one coalesced load per item. */
     const void *slot_rec;
+    /* optional static list of the (example * nchannels + channel) groups that
+     * have items (nsegs entries): the per-channel plane sort of the prepare
+     * pass (fine grids, vector typing) then launches one CTA per listed group
+     * instead of one per (example, channel). */
+    const int32_t *segs;
+    int32_t nsegs;
 } gm_batch;
 
 /* Device scratch needed by gm_prepare / gm_forward / gm_backward. */

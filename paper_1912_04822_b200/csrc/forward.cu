@@ -69,6 +69,7 @@ struct FwdArgs {
     double res;
     float resf, resl, inv_res;  // res = resf + resl
     const int4 *jobs;  // optional job table (gm_batch.fwd_jobs) or NULL
+    const int32_t *poff;  // per (example, channel) plane-bucket item offsets, or NULL
     int D, C, TI, TJ, ntj, wpp, rpw;
     int ntiles;        // tiles per (example, channel) slab
     int bulk;
@@ -238,6 +239,16 @@ __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs
     const int jg0 = j0 + part * A.rpw, jg1 = j0 + min((part + 1) * A.rpw, TJv) - 1;
     const bool region_ok = p < TIv && jg0 <= jg1;
     float *accp = acc + (size_t)p * TJ * D;  // plane p of the tile, row j at (j - j0) * D
+    if (A.poff) {
+        // items sorted by first plane (k_sort_planes): only those whose first
+        // plane lies within the channel's widest box of plane i can reach it
+        const int32_t *rec = A.poff + ((size_t)e * A.C + c) * kPlaneRec;
+        const int wmax = rec[kBuckets + 2];
+        const int b0 = plane_bucket(max(0, i - wmax + 1), D), b1 = plane_bucket(min(i, D - 1), D);
+        const int rs = rec[b0], re = rec[b1 + 1];
+        ce = cs + re;
+        cs = cs + rs;
+    }
     if (region_ok) {
         {
             const int nf = (jg1 - jg0 + 1) * D;
@@ -450,9 +461,12 @@ gm_status forward_impl(const gm_params *p, const gm_batch *b, const Workspace &w
     const FwdConfig cfg = choose_config(D);
     if (cfg.smem > 227 * 1024) return gm_fail(GM_ERR_INVALID, "grid too large for one tile row");
     FwdArgs A;
-    A.sorted = ws.sorted;
-    A.bsorted = ws.bsorted;
-    A.sbox = ws.sbox;
+    // items sorted by first plane within each channel (k_sort_planes)
+    const bool psort = use_plane_sort(p, b);
+    A.sorted = psort ? ws.psorted : ws.sorted;
+    A.bsorted = psort ? ws.pbsorted : ws.bsorted;
+    A.sbox = psort ? ws.psbox : ws.sbox;
+    A.poff = psort && kWarps == 1 ? ws.poff : nullptr;
     A.chan_off = ws.chan_off;
     A.origins = b->origins;
     A.out = out;

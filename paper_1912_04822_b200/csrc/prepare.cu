@@ -17,6 +17,14 @@
 #define GM_PREP_THREADS 64  // small blocks: the ~50k item threads spread over every SM
 #endif
 
+struct PrepArgs;
+gm_status sort_planes(const PrepArgs &A, cudaStream_t s);
+
+// per-channel plane sort (k_sort_planes, k_prepare_seg)
+constexpr int kSortThreads = 256;
+constexpr int kSortRounds = 4;
+constexpr int kSortMax = kSortThreads * kSortRounds;  // items per channel sorted in smem
+
 struct PrepArgs {
     gm_params p;
     gm_batch b;
@@ -206,23 +214,16 @@ struct CallArgs {
     double v[18 * CAP];  // origins (nex,3), then transforms (nex,15)
 };
 
+// Everything the prepare pass does for grouped slot t (static grouping):
+// transform (geom.py:105), forward record + binary record (returned), and in
+// index mode the position and the backward record (stored).
 template <int CAP>
-__global__ void __launch_bounds__(GM_PREP_THREADS) k_prepare_static(const PrepArgs A, const __grid_constant__ CallArgs<CAP> K) {
+__device__ __forceinline__ void build_slot(const PrepArgs &A, const CallArgs<CAP> &K, int t,
+                                           FwdItem &f, BinItem &bi) {
     const gm_batch &b = A.b;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int nex = K.nex;
     const bool vector = b.item_atom != nullptr;
-    if (t < 3 * nex) const_cast<double *>(b.origins)[t] = K.v[t];  // for forward / backward
-    if (t < nex * (b.nchannels + 1)) A.ws.chan_off[t] = b.chan_off[t];
-    if (vector && t < b.natoms) {  // positions of all atoms
-        const int s = b.atom_set[t];
-        const int e = b.set_example[s];
-        double x[3];
-        transform_atom_x(A, t, s, K.has_xf ? K.v + 3 * nex + 15 * e : nullptr, x);
-        store_pos(A, t, x);
-        if (b.bwd_slot) A.ws.atom_order[b.bwd_slot[t]] = t;  // vector backward launch order
-    }
-    if (!vector && b.slot_rec && t < b.nitems) {
+    if (!vector && b.slot_rec) {
         const SlotRec R = reinterpret_cast<const SlotRec *>(b.slot_rec)[t];
         const gm_params &p = A.p;
         const int D = p.npts, e = R.ex, a = R.atom;
@@ -247,7 +248,6 @@ __global__ void __launch_bounds__(GM_PREP_THREADS) k_prepare_static(const PrepAr
         axis_bounds(x[1], cut, O[1], res, D, j0, j1);
         axis_bounds(x[2], cut, O[2], res, D, k0, k1);
         const bool valid = i0 <= i1 && j0 <= j1 && k0 <= k1;
-        FwdItem f;
         split_hilo((double)i0 * res - (x[0] - O[0]), f.cxh, f.cxl);
         split_hilo((double)j0 * res - (x[1] - O[1]), f.cyh, f.cyl);
         split_hilo((double)k0 * res - (x[2] - O[2]), f.czh, f.czl);
@@ -265,9 +265,7 @@ __global__ void __launch_bounds__(GM_PREP_THREADS) k_prepare_static(const PrepAr
         f.jbox = j0 | (j1 << 16);
         f.kbox = k0 | (k1 << 16);
         f.atom = a;
-        A.ws.sorted[t] = f;
-        A.ws.sbox[t] = make_int2(f.ibox, f.jbox);
-        if (p.binary) A.ws.bsorted[t] = BinItem{x[0], x[1], x[2], __dmul_rn(r, r)};
+        bi = BinItem{x[0], x[1], x[2], __dmul_rn(r, r)};
         // the backward's record (_kernels.py:224-251 constants, same box)
         BwdAtom w;
         w.lx = x[0] - O[0];
@@ -287,7 +285,7 @@ __global__ void __launch_bounds__(GM_PREP_THREADS) k_prepare_static(const PrepAr
         w.jbox = f.jbox;
         w.kbox = f.kbox;
         A.ws.batoms[R.bslot] = w;
-    } else if (t < b.nitems) {
+    } else {
         const int it = b.item_perm[t];
         const int a = vector ? b.item_atom[it] : it;
         const int s = b.atom_set[a];
@@ -295,10 +293,32 @@ __global__ void __launch_bounds__(GM_PREP_THREADS) k_prepare_static(const PrepAr
         double x[3];
         transform_atom_x(A, a, s, K.has_xf ? K.v + 3 * nex + 15 * e : nullptr, x);
         if (!vector) store_pos(A, a, x);
-        FwdItem f;
-        BinItem bi;
         if (make_item_o(A, it, a, s, K.v + 3 * e, x, f, bi) < 0) f.ibox = 0x7fff;  // empty
         if (!vector) store_bwd_atom(A, a, e, f.ch, K.v + 3 * e, x, f);
+    }
+}
+
+
+template <int CAP>
+__global__ void __launch_bounds__(GM_PREP_THREADS) k_prepare_static(const PrepArgs A, const __grid_constant__ CallArgs<CAP> K) {
+    const gm_batch &b = A.b;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nex = K.nex;
+    const bool vector = b.item_atom != nullptr;
+    if (t < 3 * nex) const_cast<double *>(b.origins)[t] = K.v[t];  // for forward / backward
+    if (t < nex * (b.nchannels + 1)) A.ws.chan_off[t] = b.chan_off[t];
+    if (vector && t < b.natoms) {  // positions of all atoms
+        const int s = b.atom_set[t];
+        const int e = b.set_example[s];
+        double x[3];
+        transform_atom_x(A, t, s, K.has_xf ? K.v + 3 * nex + 15 * e : nullptr, x);
+        store_pos(A, t, x);
+        if (b.bwd_slot) A.ws.atom_order[b.bwd_slot[t]] = t;  // vector backward launch order
+    }
+    if (t < b.nitems) {
+        FwdItem f;
+        BinItem bi;
+        build_slot<CAP>(A, K, t, f, bi);
         A.ws.sorted[t] = f;
         A.ws.sbox[t] = make_int2(f.ibox, f.jbox);
         if (A.p.binary) A.ws.bsorted[t] = bi;
@@ -320,7 +340,7 @@ gm_status launch_static(const PrepArgs &A, const double *origins, const double *
         k_prepare_static<CAP><<<(n + GM_PREP_THREADS - 1) / GM_PREP_THREADS, GM_PREP_THREADS, 0, s>>>(A, K);
         LAUNCH_CHECK();
     }
-    return GM_OK;
+    return use_plane_sort(&A.p, &A.b) ? sort_planes(A, s) : GM_OK;
 }
 
 // One CTA per example, in phases separated by CTA barriers:
@@ -450,6 +470,151 @@ __global__ void __launch_bounds__(1024) k_prepare_example(const PrepArgs A) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Per (example, channel) stable counting sort of the grouped items by the
+// plane bucket of their box's first plane (k_forward then scans, for plane i,
+// only the items whose first plane lies within the widest box of plane i --
+// instead of every item of the channel).  One CTA per (example, channel);
+// ranks within 32-item chunks from match.any, chunk x bucket prefix tables in
+// shared memory; the order is (bucket, item order): deterministic.
+// ---------------------------------------------------------------------------
+
+template <bool SEGS>
+__global__ void __launch_bounds__(kSortThreads) k_sort_planes(const PrepArgs A) {
+    __shared__ int tab[(kSortMax / 32) * (kBuckets + 1)];  // chunk x bucket prefix
+    __shared__ int off[kBuckets + 2];
+    __shared__ int wmax_s;
+    const gm_batch &b = A.b;
+    const int C = b.nchannels, D = A.p.npts;
+    // one CTA per (example, channel) -- or per group with items when the
+    // batch lists them (gm_batch.segs; the others are zero tiles)
+    const int seg = SEGS ? b.segs[blockIdx.x] : blockIdx.x, e = seg / C, c = seg - e * C;
+    const int cs = A.ws.chan_off[(size_t)e * (C + 1) + c], ce = A.ws.chan_off[(size_t)e * (C + 1) + c + 1];
+    const int n = ce - cs;
+    int32_t *rec = A.ws.poff + (size_t)seg * kPlaneRec;
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (n <= 0) {
+        if (tid < kPlaneRec) rec[tid] = 0;
+        return;
+    }
+    const bool binary = A.p.binary;
+    const bool sortable = n <= kSortMax;
+    if (tid == 0) wmax_s = 0;
+    const int nchunk = (n + 31) >> 5;
+    if (sortable)
+        for (int t = tid; t < nchunk * (kBuckets + 1); t += kSortThreads) tab[t] = 0;
+    __syncthreads();
+    // item q = tid + round * kSortThreads: chunks of 32 consecutive items are
+    // one warp's lanes in one round
+    int key[kSortRounds], rank[kSortRounds];
+    int2 bx[kSortRounds];
+    int wloc = 0;
+    // every round's boxes in flight at once
+#pragma unroll
+    for (int r = 0; r < kSortRounds; r++) {
+        const int q = tid + r * kSortThreads;
+        bx[r] = make_int2(0x7fff, 0);
+        if (sortable && q < n) bx[r] = A.ws.sbox[cs + q];
+    }
+#pragma unroll
+    for (int r = 0; r < kSortRounds; r++) {
+        const int q = tid + r * kSortThreads;
+        key[r] = kBuckets + 1;
+        rank[r] = 0;
+        if (!sortable || r * kSortThreads >= n) continue;  // warp-uniform
+        if (q < n) {
+            const int lo = box_lo(bx[r].x), hi = box_hi(bx[r].x);
+            key[r] = lo <= hi && lo < D ? plane_bucket(lo, D) : kBuckets;
+            if (key[r] < kBuckets) wloc = max(wloc, hi - lo + 1);
+        }
+        const unsigned m = __match_any_sync(0xffffffffu, key[r]);
+        rank[r] = __popc(m & ((1u << lane) - 1u));
+        if (q < n && rank[r] == 0) tab[(q >> 5) * (kBuckets + 1) + key[r]] = __popc(m);
+    }
+    if (!sortable)
+        for (int q = tid; q < n; q += kSortThreads) {
+            const int ib = A.ws.sbox[cs + q].x;
+            if (box_lo(ib) <= box_hi(ib)) wloc = max(wloc, box_hi(ib) - box_lo(ib) + 1);
+        }
+    atomicMax(&wmax_s, wloc);
+    __syncthreads();
+    if (sortable) {
+        // per bucket: exclusive prefix over the chunks
+        if (tid <= kBuckets) {
+            int run = 0;
+            for (int k = 0; k < nchunk; k++) {
+                const int v = tab[k * (kBuckets + 1) + tid];
+                tab[k * (kBuckets + 1) + tid] = run;
+                run += v;
+            }
+            off[tid] = run;  // bucket count, scanned below
+        }
+        __syncthreads();
+        if (tid < 32) {
+            // exclusive scan of the kBuckets + 1 counts, 32 per pass
+            int carry = 0;
+            for (int b0 = 0; b0 <= kBuckets; b0 += 32) {
+                const int bk = b0 + lane;
+                const int v = bk <= kBuckets ? off[bk] : 0;
+                int sc = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, sc, o);
+                    if (lane >= o) sc += t;
+                }
+                if (bk <= kBuckets) off[bk] = carry + sc - v;
+                carry += __shfl_sync(0xffffffffu, sc, 31);
+            }
+            if (lane == 0) off[kBuckets + 1] = carry;
+        }
+        __syncthreads();
+        // all records of the thread loaded before any is stored
+        int4 rv[kSortRounds][4];
+#pragma unroll
+        for (int r = 0; r < kSortRounds; r++) {
+            const int q = tid + r * kSortThreads;
+            if (q < n) {
+                const int4 *src4 = reinterpret_cast<const int4 *>(A.ws.sorted + cs + q);
+#pragma unroll
+                for (int w4 = 0; w4 < 4; w4++) rv[r][w4] = src4[w4];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kSortRounds; r++) {
+            const int q = tid + r * kSortThreads;
+            if (q >= n) continue;
+            const int dst = cs + off[key[r]] + tab[(q >> 5) * (kBuckets + 1) + key[r]] + rank[r];
+            int4 *dst4 = reinterpret_cast<int4 *>(A.ws.psorted + dst);
+#pragma unroll
+            for (int w4 = 0; w4 < 4; w4++) dst4[w4] = rv[r][w4];
+            A.ws.psbox[dst] = bx[r];
+            if (binary) A.ws.pbsorted[dst] = A.ws.bsorted[cs + q];
+        }
+    } else {
+        for (int q = tid; q < n; q += kSortThreads) {  // unsorted: a plain copy
+            const int4 *src4 = reinterpret_cast<const int4 *>(A.ws.sorted + cs + q);
+            int4 *dst4 = reinterpret_cast<int4 *>(A.ws.psorted + cs + q);
+#pragma unroll
+            for (int w4 = 0; w4 < 4; w4++) dst4[w4] = src4[w4];
+            A.ws.psbox[cs + q] = A.ws.sbox[cs + q];
+            if (binary) A.ws.pbsorted[cs + q] = A.ws.bsorted[cs + q];
+        }
+    }
+    if (tid <= kBuckets + 1) rec[tid] = sortable ? off[tid] : (tid == 0 ? 0 : n);
+    if (tid == 0) rec[kBuckets + 2] = sortable ? wmax_s : D;  // unsorted: scan everything
+}
+
+gm_status sort_planes(const PrepArgs &A, cudaStream_t s) {
+    const int nseg = A.b.nexamples * A.b.nchannels;
+    if (A.b.segs) {
+        if (A.b.nsegs > 0) k_sort_planes<true><<<A.b.nsegs, kSortThreads, 0, s>>>(A);
+    } else if (nseg > 0) {
+        k_sort_planes<false><<<nseg, kSortThreads, 0, s>>>(A);
+    }
+    LAUNCH_CHECK();
+    return GM_OK;
+}
+
 gm_status prepare_impl(const gm_params *p, const gm_batch *b, const Workspace &ws,
                        cudaStream_t s, bool items_too) {
     PrepArgs A;
@@ -480,7 +645,7 @@ gm_status prepare_impl(const gm_params *p, const gm_batch *b, const Workspace &w
         k_prepare_example<false><<<b->nexamples, 1024, base, s>>>(A);
     }
     LAUNCH_CHECK();
-    return GM_OK;
+    return use_plane_sort(&A.p, &A.b) ? sort_planes(A, s) : GM_OK;
 }
 
 // Per-call arrays from host memory (see gm_prepare_inline).

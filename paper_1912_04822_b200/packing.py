@@ -197,6 +197,11 @@ class PackedBatch:
         chan_off = np.searchsorted(key[perm], bounds.reshape(-1), side="left").astype(np.int32)
         L.add("item_perm", perm)
         L.add("chan_off", chan_off)
+        # groups (example * nchannels + channel) that have items (gm_batch.segs)
+        segs = np.nonzero(np.diff(chan_off.reshape(self.nexamples, -1), axis=1).reshape(-1) > 0)[0] \
+            if self.nexamples else np.zeros(0, np.int64)
+        self.nsegs = int(segs.shape[0])
+        L.add("segs", segs.astype(np.int32))
         if not self.vector_mode and self.nitems:
             # index mode: per-slot records (gm_batch.slot_rec), item_perm order
             rec = np.zeros(self.nitems, _SLOT_DTYPE)
@@ -356,11 +361,12 @@ class PackedBatch:
             b.vector_mode = int(self.vector_mode)
             b.nweights = self.nweights
             b.max_example_items = self.max_example_items
+            b.nsegs = self.nsegs
             for name in ("coords32", "atom_radius", "atom_set", "atom_type", "set_start",
                          "set_end", "set_example", "set_choff", "set_t", "set_wstart", "weights",
                          "type_radius", "set_trstart", "item_atom", "item_channel",
                          "item_weight", "item_radius", "ex_item_start", "ex_item_end",
-                         "item_perm", "chan_off", "bwd_slot", "slot_rec"):
+                         "item_perm", "chan_off", "bwd_slot", "slot_rec", "segs"):
                 setattr(b, name, self.ptr(name))
             base = self._percall.data_ptr()
             b.origins = base
