@@ -455,6 +455,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
                         }
                         __syncwarp();
                         // ---- phase 2: kU windows of 32 voxels per step ----
+                        // grid_grad may come from the previous kernel (PDL launch):
+                        // the prologue above overlapped it, the loads must not
+                        pdl_wait();
                         int cur = -1;  // rows started before the next window, minus one
                         const int last = total - 1;
                         for (int base = 0; base < total; base += 32 * kU) {
@@ -668,7 +671,8 @@ gm_status backward_impl(const gm_params *p, const gm_batch *b, const Workspace &
     if (b->vector_mode)
         k_backward_vector<<<(b->natoms + kBwdWarps - 1) / kBwdWarps, kBwdWarps * 32, 0, s>>>(P);
     else
-        k_backward_index<<<(b->natoms + kBwdWarps - 1) / kBwdWarps, kBwdWarps * 32, 0, s>>>(P);
+        CUDA_TRY(gm_launch_pdl(k_backward_index, dim3((b->natoms + kBwdWarps - 1) / kBwdWarps),
+                               dim3(kBwdWarps * 32), 0, s, P));
     LAUNCH_CHECK();
     return GM_OK;
 }

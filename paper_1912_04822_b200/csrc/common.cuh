@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <utility>
 
 #include "../../include/gridmaker_b200.h"
 
@@ -160,6 +161,42 @@ __device__ __forceinline__ void axis_bounds(double x, double cut, double origin,
     h = fmax(fmin(h, (double)(D - 1)), -1.0);
     lo = (int)l;
     hi = (int)h;
+}
+
+// Programmatic dependent launch (PDL): a kernel launched with
+// gm_launch_pdl may start while the previous kernel of the stream drains;
+// pdl_wait() blocks until that kernel has completed and its writes are
+// visible.  pdl_trigger() lets the next PDL-launched kernel start; our kernels
+// call it only after their own pdl_wait(), so everything before the previous
+// kernel (e.g. the prepare pass) is complete when a dependent starts.
+#ifndef GM_PDL
+#define GM_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if GM_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger() {
+#if GM_PDL
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t gm_launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                          cudaStream_t s, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = GM_PDL ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {

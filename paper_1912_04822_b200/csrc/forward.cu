@@ -167,6 +167,10 @@ template <bool BINARY, bool VECTOR, bool RESL>
 __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs A) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // the prepare pass's records must be complete; then the backward (next in
+    // the stream) may begin its prologue while this grid drains
+    pdl_wait();
+    pdl_trigger();
     // grid (channel, tile, example): consecutive CTAs are the channels of one
     // tile, so scatter work and zero-tile stores interleave finely, which
     // keeps HBM writing while SMs compute
@@ -442,13 +446,13 @@ gm_status launch(const FwdArgs &A, const FwdConfig &cfg, int nex, int njobs, cud
     auto kern = k_forward<BIN, VEC, RESL>;
     CUDA_TRY(gm_ensure_smem((const void *)kern, (int)cfg.smem));
     if (A.jobs) {
-        if (njobs > 0) kern<<<njobs, kThreads, cfg.smem, s>>>(A);
+        if (njobs > 0) CUDA_TRY(gm_launch_pdl(kern, dim3(njobs), dim3(kThreads), cfg.smem, s, A));
         LAUNCH_CHECK();
         return GM_OK;
     }
     if (A.ntiles > 65535 || nex > 65535) return gm_fail(GM_ERR_INVALID, "too many examples or tiles");
     dim3 grid(A.C, A.ntiles, nex);
-    kern<<<grid, kThreads, cfg.smem, s>>>(A);
+    CUDA_TRY(gm_launch_pdl(kern, grid, dim3(kThreads), cfg.smem, s, A));
     LAUNCH_CHECK();
     return GM_OK;
 }
