@@ -94,8 +94,8 @@ typedef struct {
      * one fully parallel pass. */
     const int32_t *item_perm;
     const int32_t *chan_off;
-    /* optional forward job table (device, 4 int32 per job: example * nchannels +
-     * channel, tile, static item range begin, end), built by gm_forward_jobs
+    /* optional forward job table (device, 4 int32 per job: example, channel,
+     * tile, first plane | first row << 16), built by gm_forward_jobs
      * from the static chan_off for grids of fwd_jobs_npts points per side: only
      * tiles of channels with items plus one job per group of zero tiles are
      * launched (the kernel re-reads the item ranges of the prepare pass, so the

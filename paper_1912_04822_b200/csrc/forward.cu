@@ -174,24 +174,29 @@ __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs
     // grid (channel, tile, example): consecutive CTAs are the channels of one
     // tile, so scatter work and zero-tile stores interleave finely, which
     // keeps HBM writing while SMs compute
-    int tile, e, c, cs, ce;
+    int tile, e, c, cs, ce, i0, j0;
+    const int D = A.D, TI = A.TI, TJ = A.TJ;
     if (A.jobs) {
-        // job table: only tiles with items, one job per group of zero tiles.
-        // The item range is re-read from the prepare pass (a static channel
-        // with items may still lose them all to the grid's bounds).
-        const int2 j = *reinterpret_cast<const int2 *>(A.jobs + blockIdx.x);
-        e = j.x / A.C;
-        c = j.x - e * A.C;
-        tile = j.y;
+        // job table: only tiles with items, one job per group of zero tiles;
+        // {example, channel, tile, first plane | first row << 16}: no integer
+        // division before the first load.  The item range is re-read from the
+        // prepare pass (a static channel with items may still lose them all
+        // to the grid's bounds).
+        const int4 j = A.jobs[blockIdx.x];
+        e = j.x;
+        c = j.y;
+        tile = j.z;
+        i0 = j.w & 0xffff;
+        j0 = j.w >> 16;
     } else {
         tile = blockIdx.y;
         e = blockIdx.z;
         c = blockIdx.x;
+        i0 = (tile / A.ntj) * TI;
+        j0 = (tile % A.ntj) * TJ;
     }
     cs = A.chan_off[(size_t)e * (A.C + 1) + c];
     ce = A.chan_off[(size_t)e * (A.C + 1) + c + 1];
-    const int D = A.D, TI = A.TI, TJ = A.TJ;
-    const int i0 = (tile / A.ntj) * TI, j0 = (tile % A.ntj) * TJ;
     const int TIv = min(TI, D - i0), TJv = min(TJ, D - j0);
     const size_t plane = (size_t)D * D;
     float *obase = A.out + ((size_t)e * A.C + c) * D * plane + (size_t)i0 * plane + (size_t)j0 * D;
@@ -525,7 +530,7 @@ int32_t forward_jobs_impl(const gm_params *p, int32_t nex, int32_t nch, const in
                 }
             }
     const long long n = (long long)work.size() + (long long)zero.size();
-    if (n > 0x7fffffffLL) return -1;
+    if (n > 0x7fffffffLL || D > 0x7fff) return -1;  // plane | row << 16 must fit
     if (jobs && D <= GM_FWD_LPT_MAXD) {
 #if GM_FWD_LPT
         // heaviest first within groups of GM_FWD_LPT_GROUP examples (0: globally)
@@ -570,10 +575,10 @@ int32_t forward_jobs_impl(const gm_params *p, int32_t nex, int32_t nch, const in
 #endif
             const Job &j = z ? zero[zi++] : work[wi++];
             int32_t *o = jobs + 4 * k;
-            o[0] = j.slab;
-            o[1] = j.tile;
-            o[2] = j.cs;
-            o[3] = j.ce;
+            o[0] = j.slab / nch;  // example
+            o[1] = j.slab % nch;  // channel
+            o[2] = j.tile;
+            o[3] = ((j.tile / ntj) * cfg.TI) | (((j.tile % ntj) * cfg.TJ) << 16);
         }
     }
     return (int32_t)n;
