@@ -163,6 +163,146 @@ __device__ __forceinline__ bool plan_visit(const FwdItem &it, int i, int jg0, in
     return true;
 }
 
+// Phases A/B of one warp region: the channel's items [cs, ce) scattered, in
+// order, into plane i, rows [jg0, jg1] of the accumulator (accp: plane i of
+// the tile, row j at (j - j0) * D).
+template <bool BINARY, bool VECTOR, bool RESL>
+__device__ __forceinline__ void scatter_items(const FwdArgs &A, float *accp, Slot *slots, int lane,
+                                              int e, int i, int jg0, int jg1, int j0, int cs,
+                                              int ce) {
+    const int D = A.D;
+    const double res = A.res;
+    const float resf = A.resf, resl = A.resl, inv_res = A.inv_res;
+    const double ox = A.origins[3 * e + 0], oy = A.origins[3 * e + 1],
+                 oz = A.origins[3 * e + 2];
+    // the next chunk's records are prefetched into registers while the
+    // current chunk scatters (hides the L2 latency of phase A)
+    FwdItem nxt;
+    int2 nbox = make_int2(1, 0);  // empty box
+    if (cs + lane < ce) {
+        nbox = A.sbox[cs + lane];
+        nxt = A.sorted[cs + lane];
+    }
+    for (int base = cs; base < ce; base += 32) {
+        // ---- phase A: lane t plans item base + t ----
+        const int it = base + lane;
+        const FwdItem cur_item = nxt;
+        const int2 bx = nbox;
+        nbox = make_int2(1, 0);
+        if (it + 32 < ce) {
+            nbox = A.sbox[it + 32];
+            nxt = A.sorted[it + 32];
+        }
+        bool hit = false;
+        if (it < ce && box_lo(bx.x) <= i && box_hi(bx.x) >= i && box_lo(bx.y) <= jg1 &&
+            box_hi(bx.y) >= jg0) {
+            Slot S;
+            hit = plan_visit(cur_item, i, jg0, jg1, j0, D, resf, resl, inv_res, S);
+            if (hit) {
+                S.src = it;
+                slots[lane] = S;
+            }
+        }
+        unsigned m = __ballot_sync(0xffffffffu, hit);
+        __syncwarp();
+        // ---- phase B: items in order, all lanes scatter ----
+        while (m) {
+            const int t = __ffs(m) - 1;
+            m &= m - 1;
+            const float4 S0 = *reinterpret_cast<const float4 *>(&slots[t].yh);
+            const float4 S1 = *reinterpret_cast<const float4 *>(&slots[t].dx2);
+            const float4 S2 = *reinterpret_cast<const float4 *>(&slots[t].qa);
+            const int4 S3 = *reinterpret_cast<const int4 *>(&slots[t].arow);
+            const int jr0 = box_lo(__float_as_int(S2.z)), nj = box_hi(__float_as_int(S2.z));
+            const int kr0 = box_lo(__float_as_int(S2.w)), nk = box_hi(__float_as_int(S2.w));
+            const int nks = S3.y;
+            const float inv = __int_as_float(S3.w);  // 1/nks (approximate, exact enough)
+            const int r = small_div(lane, inv), rpi = small_div(32, inv);
+            if (BINARY) {
+                // _kernels.py:87-98 (index) / 180-192 (vector): exact f64, no contraction
+                const BinItem bi = A.bsorted[S3.z];
+                const int4 bx = *reinterpret_cast<const int4 *>(&A.sorted[S3.z].ibox);
+                const int jb = box_lo(bx.y) + jr0, kb0 = box_lo(bx.z) + kr0;
+                const double dxd =
+                    __dsub_rn(__dadd_rn(ox, __dmul_rn((double)i, res)), bi.x);
+                const double dx2 = __dmul_rn(dxd, dxd);
+                const float w = S2.y;
+                for (int kb = 0; kb < nk; kb += 32) {
+                    const int nkb = min(32, nk - kb);
+                    const float invb = __frcp_rn((float)nkb);
+                    const int rpb = small_div(32, invb);
+                    const int rr = small_div(lane, invb), kk = kb + lane - rr * nkb;
+                    if (rr >= rpb) continue;
+                    const double dz =
+                        __dsub_rn(__dadd_rn(oz, __dmul_rn((double)(kb0 + kk), res)), bi.z);
+                    const double dz2 = __dmul_rn(dz, dz);
+                    float *ap = accp + S3.x + kr0 + kk + (size_t)rr * D;
+                    for (int jj = rr; jj < nj; jj += rpb, ap += (size_t)rpb * D) {
+                        const double dy = __dsub_rn(
+                            __dadd_rn(oy, __dmul_rn((double)(jb + jj), res)), bi.y);
+                        const double d2 = __dadd_rn(__dadd_rn(dx2, __dmul_rn(dy, dy)), dz2);
+                        if (d2 <= bi.r2) {
+                            if (VECTOR) *ap = fmaxf(*ap, w);
+                            else *ap = 1.0f;
+                        }
+                    }
+                }
+            } else if (nk <= 32) {
+                // _kernels.py:99-106: Gaussian core to d0, quadratic tail to the cutoff
+                if (r < rpi) {
+                    const int kk = kr0 + lane - r * nks;
+                    const float fk = (float)kk;
+                    const float dz = fmaf(fk, resf, S0.z) + fmaf(fk, resl, S0.w);
+                    const float b2 = fmaf(dz, dz, S1.x);
+                    const float cexp = S1.y, d02 = S1.z, cut = S1.w, qa = S2.x, w = S2.y;
+                    const float rpif = (float)rpi;
+                    float *ap = accp + S3.x + kk + r * D;
+                    const int step = rpi * D;
+                    float jf = (float)(jr0 + r);
+                    auto val = [&](float y) {
+                        const float dy = RESL ? fmaf(y, resf, S0.x) + fmaf(y, resl, S0.y)
+                                              : fmaf(y, resf, S0.x) + S0.y;
+                        const float d2 = fmaf(dy, dy, b2);
+                        const float g = fast_ex2(d2 * cexp);
+                        const float t2 = fmaxf(cut - fast_sqrt(d2), 0.0f);
+                        return d2 <= d02 ? g : qa * t2 * t2;
+                    };
+                    int jj = r;
+                    // two rows per iteration: both accumulator reads are
+                    // issued before either write (different rows)
+                    for (; jj + rpi < nj; jj += 2 * rpi, jf += 2.0f * rpif, ap += 2 * step) {
+                        const float v0 = val(jf), v1 = val(jf + rpif);
+                        const float a0 = ap[0], a1 = ap[step];
+                        ap[0] = fmaf(w, v0, a0);
+                        ap[step] = fmaf(w, v1, a1);
+                    }
+                    if (jj < nj) *ap = fmaf(w, val(jf), *ap);
+                }
+            } else {
+                // > 32 columns (very fine grids): one row pass per 32 columns
+                const float cexp = S1.y, d02 = S1.z, cut = S1.w, qa = S2.x, w = S2.y;
+                for (int kb = lane; kb < nk; kb += 32) {
+                    const int kk = kr0 + kb;
+                    const float fk = (float)kk;
+                    const float dz = fmaf(fk, resf, S0.z) + fmaf(fk, resl, S0.w);
+                    const float b2 = fmaf(dz, dz, S1.x);
+                    float *ap = accp + S3.x + kk;
+                    for (int jj = 0; jj < nj; jj++, ap += D) {
+                        const float jf = (float)(jr0 + jj);
+                        const float dy = fmaf(jf, resf, S0.x) + fmaf(jf, resl, S0.y);
+                        const float d2 = fmaf(dy, dy, b2);
+                        const float g = fast_ex2(d2 * cexp);
+                        const float t2 = fmaxf(cut - fast_sqrt(d2), 0.0f);
+                        const float v = d2 <= d02 ? g : qa * t2 * t2;
+                        *ap = fmaf(w, v, *ap);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
 template <bool BINARY, bool VECTOR, bool RESL>
 __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs A) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -270,136 +410,7 @@ __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs
                 for (int q = lane; q < nf; q += 32) rs[q] = 0.0f;
             }
         }
-        const double res = A.res;
-        const float resf = A.resf, resl = A.resl, inv_res = A.inv_res;
-        const double ox = A.origins[3 * e + 0], oy = A.origins[3 * e + 1],
-                     oz = A.origins[3 * e + 2];
-        // the next chunk's records are prefetched into registers while the
-        // current chunk scatters (hides the L2 latency of phase A)
-        FwdItem nxt;
-        int2 nbox = make_int2(1, 0);  // empty box
-        if (cs + lane < ce) {
-            nbox = A.sbox[cs + lane];
-            nxt = A.sorted[cs + lane];
-        }
-        for (int base = cs; base < ce; base += 32) {
-            // ---- phase A: lane t plans item base + t ----
-            const int it = base + lane;
-            const FwdItem cur_item = nxt;
-            const int2 bx = nbox;
-            nbox = make_int2(1, 0);
-            if (it + 32 < ce) {
-                nbox = A.sbox[it + 32];
-                nxt = A.sorted[it + 32];
-            }
-            bool hit = false;
-            if (it < ce && box_lo(bx.x) <= i && box_hi(bx.x) >= i && box_lo(bx.y) <= jg1 &&
-                box_hi(bx.y) >= jg0) {
-                Slot S;
-                hit = plan_visit(cur_item, i, jg0, jg1, j0, D, resf, resl, inv_res, S);
-                if (hit) {
-                    S.src = it;
-                    slots[lane] = S;
-                }
-            }
-            unsigned m = __ballot_sync(0xffffffffu, hit);
-            __syncwarp();
-            // ---- phase B: items in order, all lanes scatter ----
-            while (m) {
-                const int t = __ffs(m) - 1;
-                m &= m - 1;
-                const float4 S0 = *reinterpret_cast<const float4 *>(&slots[t].yh);
-                const float4 S1 = *reinterpret_cast<const float4 *>(&slots[t].dx2);
-                const float4 S2 = *reinterpret_cast<const float4 *>(&slots[t].qa);
-                const int4 S3 = *reinterpret_cast<const int4 *>(&slots[t].arow);
-                const int jr0 = box_lo(__float_as_int(S2.z)), nj = box_hi(__float_as_int(S2.z));
-                const int kr0 = box_lo(__float_as_int(S2.w)), nk = box_hi(__float_as_int(S2.w));
-                const int nks = S3.y;
-                const float inv = __int_as_float(S3.w);  // 1/nks (approximate, exact enough)
-                const int r = small_div(lane, inv), rpi = small_div(32, inv);
-                if (BINARY) {
-                    // _kernels.py:87-98 (index) / 180-192 (vector): exact f64, no contraction
-                    const BinItem bi = A.bsorted[S3.z];
-                    const int4 bx = *reinterpret_cast<const int4 *>(&A.sorted[S3.z].ibox);
-                    const int jb = box_lo(bx.y) + jr0, kb0 = box_lo(bx.z) + kr0;
-                    const double dxd =
-                        __dsub_rn(__dadd_rn(ox, __dmul_rn((double)i, res)), bi.x);
-                    const double dx2 = __dmul_rn(dxd, dxd);
-                    const float w = S2.y;
-                    for (int kb = 0; kb < nk; kb += 32) {
-                        const int nkb = min(32, nk - kb);
-                        const float invb = __frcp_rn((float)nkb);
-                        const int rpb = small_div(32, invb);
-                        const int rr = small_div(lane, invb), kk = kb + lane - rr * nkb;
-                        if (rr >= rpb) continue;
-                        const double dz =
-                            __dsub_rn(__dadd_rn(oz, __dmul_rn((double)(kb0 + kk), res)), bi.z);
-                        const double dz2 = __dmul_rn(dz, dz);
-                        float *ap = accp + S3.x + kr0 + kk + (size_t)rr * D;
-                        for (int jj = rr; jj < nj; jj += rpb, ap += (size_t)rpb * D) {
-                            const double dy = __dsub_rn(
-                                __dadd_rn(oy, __dmul_rn((double)(jb + jj), res)), bi.y);
-                            const double d2 = __dadd_rn(__dadd_rn(dx2, __dmul_rn(dy, dy)), dz2);
-                            if (d2 <= bi.r2) {
-                                if (VECTOR) *ap = fmaxf(*ap, w);
-                                else *ap = 1.0f;
-                            }
-                        }
-                    }
-                } else if (nk <= 32) {
-                    // _kernels.py:99-106: Gaussian core to d0, quadratic tail to the cutoff
-                    if (r < rpi) {
-                        const int kk = kr0 + lane - r * nks;
-                        const float fk = (float)kk;
-                        const float dz = fmaf(fk, resf, S0.z) + fmaf(fk, resl, S0.w);
-                        const float b2 = fmaf(dz, dz, S1.x);
-                        const float cexp = S1.y, d02 = S1.z, cut = S1.w, qa = S2.x, w = S2.y;
-                        const float rpif = (float)rpi;
-                        float *ap = accp + S3.x + kk + r * D;
-                        const int step = rpi * D;
-                        float jf = (float)(jr0 + r);
-                        auto val = [&](float y) {
-                            const float dy = RESL ? fmaf(y, resf, S0.x) + fmaf(y, resl, S0.y)
-                                                  : fmaf(y, resf, S0.x) + S0.y;
-                            const float d2 = fmaf(dy, dy, b2);
-                            const float g = fast_ex2(d2 * cexp);
-                            const float t2 = fmaxf(cut - fast_sqrt(d2), 0.0f);
-                            return d2 <= d02 ? g : qa * t2 * t2;
-                        };
-                        int jj = r;
-                        // two rows per iteration: both accumulator reads are
-                        // issued before either write (different rows)
-                        for (; jj + rpi < nj; jj += 2 * rpi, jf += 2.0f * rpif, ap += 2 * step) {
-                            const float v0 = val(jf), v1 = val(jf + rpif);
-                            const float a0 = ap[0], a1 = ap[step];
-                            ap[0] = fmaf(w, v0, a0);
-                            ap[step] = fmaf(w, v1, a1);
-                        }
-                        if (jj < nj) *ap = fmaf(w, val(jf), *ap);
-                    }
-                } else {
-                    // > 32 columns (very fine grids): one row pass per 32 columns
-                    const float cexp = S1.y, d02 = S1.z, cut = S1.w, qa = S2.x, w = S2.y;
-                    for (int kb = lane; kb < nk; kb += 32) {
-                        const int kk = kr0 + kb;
-                        const float fk = (float)kk;
-                        const float dz = fmaf(fk, resf, S0.z) + fmaf(fk, resl, S0.w);
-                        const float b2 = fmaf(dz, dz, S1.x);
-                        float *ap = accp + S3.x + kk;
-                        for (int jj = 0; jj < nj; jj++, ap += D) {
-                            const float jf = (float)(jr0 + jj);
-                            const float dy = fmaf(jf, resf, S0.x) + fmaf(jf, resl, S0.y);
-                            const float d2 = fmaf(dy, dy, b2);
-                            const float g = fast_ex2(d2 * cexp);
-                            const float t2 = fmaxf(cut - fast_sqrt(d2), 0.0f);
-                            const float v = d2 <= d02 ? g : qa * t2 * t2;
-                            *ap = fmaf(w, v, *ap);
-                        }
-                    }
-                }
-                __syncwarp();
-            }
-        }
+        scatter_items<BINARY, VECTOR, RESL>(A, accp, slots, lane, e, i, jg0, jg1, j0, cs, ce);
     }
 
     // ---- the finished tile, zeros included ----
@@ -451,7 +462,9 @@ gm_status launch(const FwdArgs &A, const FwdConfig &cfg, int nex, int njobs, cud
     auto kern = k_forward<BIN, VEC, RESL>;
     CUDA_TRY(gm_ensure_smem((const void *)kern, (int)cfg.smem));
     if (A.jobs) {
-        if (njobs > 0) CUDA_TRY(gm_launch_pdl(kern, dim3(njobs), dim3(kThreads), cfg.smem, s, A));
+        if (njobs > 0) {
+            CUDA_TRY(gm_launch_pdl(kern, dim3(njobs), dim3(kThreads), cfg.smem, s, A));
+        }
         LAUNCH_CHECK();
         return GM_OK;
     }
