@@ -175,7 +175,7 @@ __device__ __forceinline__ void store_coord(const BwdArgs &P, int a, int lane, d
 #endif
 constexpr int kBwdWarps = GM_BWD_WARPS;
 #ifndef GM_BWD_ROWS
-#define GM_BWD_ROWS 64
+#define GM_BWD_ROWS 96
 #endif
 #ifndef GM_BWD_KU
 #define GM_BWD_KU 4
