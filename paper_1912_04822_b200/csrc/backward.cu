@@ -31,7 +31,6 @@ struct BwdArgs {
     const float *grid_grad;
     float *coord_grad;
     float *type_grad;
-    const FwdItem *items;  // index mode: item a == atom a; its box (cut rmult*r) is reused
     const BwdAtom *batoms; // index mode: per-atom records of the prepare pass
     const int32_t *atom_order; // vector mode: atom of each launch slot (bwd_slot inverse)
     double eg;             // exp(-2 grm^2), a batch constant (_kernels.py:224)
@@ -664,7 +663,6 @@ gm_status backward_impl(const gm_params *p, const gm_batch *b, const Workspace &
     P.grid_grad = grid_grad;
     P.coord_grad = coord_grad;
     P.type_grad = type_grad;
-    P.items = ws.items;
     P.batoms = ws.batoms;
     P.atom_order = ws.atom_order;
     P.eg = exp((-2.0 * p->gaussian_radius_multiple) * p->gaussian_radius_multiple);

@@ -308,3 +308,41 @@ def test_vector_item_windex_maps_items_to_weight_rows():
     assert pb.item_windex.shape == (pb.nitems,)
     np.testing.assert_array_equal(host["weights"][pb.item_windex], host["item_weight"])
     assert pb.atom_example.shape == (pb.natoms,)
+
+
+def test_forward_job_table_covers_every_tile_once():
+    """gm_forward_jobs (host side of the C ABI): every tile of a channel with
+    items exactly once, one job per GM_FWD_ZGROUP group of a zero slab, the
+    (plane, row) field consistent with the tile index."""
+    import ctypes
+
+    from paper_1912_04822_b200 import GridMaker, _native, synthetic
+    from paper_1912_04822_b200.packing import PackedBatch
+
+    exs = synthetic.batch(3, seed=2)
+    pb = PackedBatch([ex.coord_sets for ex in exs], 28, False, 1.0, False, "cpu")
+    lib = _native.load_library()
+    for res, dim in ((0.5, 23.5), (0.25, 23.75)):
+        gm = GridMaker(resolution=res, dimension=dim)
+        D = gm.points_per_side()
+        p = gm._gm_params(D)
+        off = pb.offsets["chan_off"][0]
+        n = pb.nexamples * (pb.nchannels + 1)
+        co = np.ascontiguousarray(pb.host.numpy()[off:off + 4 * n].view(np.int32))
+        cnt = lib.gm_forward_jobs(ctypes.byref(p), 3, 28, co.ctypes.data, None, 0)
+        jobs = np.zeros((cnt, 4), np.int32)
+        assert lib.gm_forward_jobs(ctypes.byref(p), 3, 28, co.ctypes.data, jobs.ctypes.data,
+                                   cnt) == cnt
+        co2 = co.reshape(3, 29)
+        nonzero = {(e, c) for e in range(3) for c in range(28) if co2[e, c + 1] > co2[e, c]}
+        seen = {}
+        for e, c, t, ij in jobs:
+            seen.setdefault((e, c), []).append(t)
+            assert 0 <= ij & 0xffff < D and 0 <= ij >> 16 < D
+        ntiles = max(max(v) for v in seen.values()) + 1
+        for (e, c), ts in seen.items():
+            if (e, c) in nonzero:
+                assert sorted(ts) == list(range(ntiles))
+            else:
+                assert ts and all(t % 8 == 0 for t in ts)
+        assert len(seen) == 3 * 28
