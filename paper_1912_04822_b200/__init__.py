@@ -12,7 +12,8 @@ from .errors import ConfigError, DeviceError, FormatError, VoxmolError
 from .export import read_npy, write_npy
 from .geom import (IDENTITY_QUATERNION, Quaternion, Transform, draw_transforms,
                    make_transform, random_unit_quaternion, transform_example)
-from .voxelizer import GridMaker, channel_count, channel_names, save_grid
+from .voxelizer import (GridMaker, channel_count, channel_names, get_num_threads, save_grid,
+                        set_num_threads)
 
 __version__ = "0.1.0"
 
@@ -20,5 +21,5 @@ __all__ = [
     "CoordinateSet", "Example", "make_vector_types", "ConfigError", "DeviceError",
     "VoxmolError", "FormatError", "read_npy", "write_npy", "IDENTITY_QUATERNION", "Quaternion", "Transform", "draw_transforms",
     "make_transform", "random_unit_quaternion", "transform_example", "GridMaker",
-    "channel_count", "channel_names", "save_grid",
+    "channel_count", "channel_names", "save_grid", "set_num_threads", "get_num_threads",
 ]

@@ -34,6 +34,27 @@ from .packing import PackedBatch, stream_handle
 from .validation import check_rng, check_vector3
 
 
+_HOST_THREADS = [max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+                       else (os.cpu_count() or 1))]
+
+
+def set_num_threads(n: int) -> int:
+    """voxelizer.py:33-46: same validation and return value.  The gridding
+    runs on the GPU; the count bounds the host threads of this process's
+    numpy/torch work (torch.set_num_threads) and is returned as in effect."""
+    n = int(n)
+    if n < 1:
+        raise ValueError("thread count must be >= 1")
+    _HOST_THREADS[0] = min(n, max(1, os.cpu_count() or 1))
+    torch.set_num_threads(_HOST_THREADS[0])
+    return _HOST_THREADS[0]
+
+
+def get_num_threads() -> int:
+    """voxelizer.py:49-52."""
+    return _HOST_THREADS[0]
+
+
 def channel_count(example) -> int:
     """Total channels of an example: sum of its sets' type counts."""
     return sum(int(cs.num_types) for cs in coord_sets_of(example))

@@ -346,3 +346,18 @@ def test_forward_job_table_covers_every_tile_once():
             else:
                 assert ts and all(t % 8 == 0 for t in ts)
         assert len(seen) == 3 * 28
+
+
+def test_thread_control_api():
+    """set_num_threads / get_num_threads (voxelizer.py:33-52): validation and
+    the returned count."""
+    import pytest
+
+    from paper_1912_04822_b200 import get_num_threads, set_num_threads
+
+    n0 = get_num_threads()
+    assert n0 >= 1
+    assert set_num_threads(1) == 1 == get_num_threads()
+    with pytest.raises(ValueError):
+        set_num_threads(0)
+    set_num_threads(n0)
