@@ -323,3 +323,34 @@ def test_job_table_with_dynamic_grouping_path():
     ref = go.forward_batch(exs, random_rotation=True, random_translation=2.0,
                            rng=np.random.default_rng(6))
     assert_close(grid, ref, what="205-example batch")
+
+
+@pytest.mark.parametrize("vector,res,dim", [(False, 0.5, 23.5), (True, 0.5, 23.5),
+                                            (False, 0.25, 23.75)])
+def test_channels_whose_items_all_miss_the_grid(vector, res, dim):
+    """A set whose atoms all lie outside the grid: its channels have items in
+    the static grouping but none reaches a voxel (empty boxes), under the job
+    table, the plane sort and the backward launch order."""
+    from paper_1912_04822_b200 import Example, GridMaker, synthetic
+
+    rng = np.random.default_rng(41)
+    exs = []
+    for _ in range(3):
+        far = synthetic.receptor(rng, 60, 3.0, offset=np.array([80.0, -75.0, 90.0]))
+        lig = synthetic.ligand(rng, 12, 3.0)
+        if vector:
+            far, lig = synthetic.vectorize(far, rng), synthetic.vectorize(lig, rng)
+        exs.append(Example(coord_sets=[far, lig], labels=[0.0]))
+    gm = GridMaker(resolution=res, dimension=dim)
+    grid, xf = gm.forward_batch(exs, random_rotation=True, random_translation=1.0,
+                                rng=np.random.default_rng(2), return_transforms=True)
+    go = oracle.GridOracle(resolution=res, dimension=dim)
+    ref = go.forward_batch(exs, random_rotation=True, random_translation=1.0,
+                           rng=np.random.default_rng(2))
+    assert not grid[:, :14].any()
+    assert_close(grid, ref, what="far-set batch")
+    got = gm.backward_batch(exs, ref, transforms=xf)
+    cgs, tgs = go.backward_batch(exs, ref, random_rotation=True, random_translation=1.0,
+                                 rng=np.random.default_rng(2))
+    assert_close(np.concatenate([c for ex in got for (c, _) in ex]), np.concatenate(cgs),
+                 what="far-set backward")
