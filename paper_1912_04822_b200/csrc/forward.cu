@@ -219,29 +219,45 @@ __device__ __forceinline__ void scatter_items(const FwdArgs &A, float *accp, Slo
             const float inv = __int_as_float(S3.w);  // 1/nks (approximate, exact enough)
             const int r = small_div(lane, inv), rpi = small_div(32, inv);
             if (BINARY) {
-                // _kernels.py:87-98 (index) / 180-192 (vector): exact f64, no contraction
-                const BinItem bi = A.bsorted[S3.z];
-                const int4 bx = *reinterpret_cast<const int4 *>(&A.sorted[S3.z].ibox);
-                const int jb = box_lo(bx.y) + jr0, kb0 = box_lo(bx.z) + kr0;
-                const double dxd =
-                    __dsub_rn(__dadd_rn(ox, __dmul_rn((double)i, res)), bi.x);
-                const double dx2 = __dmul_rn(dxd, dxd);
+                // _kernels.py:87-98 (index) / 180-192 (vector): the occupancy test
+                // d^2 <= r^2 decided like the reference's f64 expression.  The f32
+                // distance from the hi/lo offsets is within ~1e-5 A^2 of it, so
+                // outside a band of 1e-4 (r^2 + 1 A^2) around r^2 its answer is
+                // the reference's; inside the band (rare) the exact f64
+                // expression, same association, no contraction, decides.
                 const float w = S2.y;
+                const float r2f = S1.w * S1.w;  // cut = r in binary mode
+                const float band = 1e-4f * (r2f + 1.0f);
+                const float lo2 = r2f - band, hi2 = r2f + band;
                 for (int kb = 0; kb < nk; kb += 32) {
                     const int nkb = min(32, nk - kb);
                     const float invb = __frcp_rn((float)nkb);
                     const int rpb = small_div(32, invb);
                     const int rr = small_div(lane, invb), kk = kb + lane - rr * nkb;
                     if (rr >= rpb) continue;
-                    const double dz =
-                        __dsub_rn(__dadd_rn(oz, __dmul_rn((double)(kb0 + kk), res)), bi.z);
-                    const double dz2 = __dmul_rn(dz, dz);
+                    const float fk = (float)(kr0 + kk);
+                    const float dzf = fmaf(fk, resf, S0.z) + fmaf(fk, resl, S0.w);
+                    const float b2f = fmaf(dzf, dzf, S1.x);
                     float *ap = accp + S3.x + kr0 + kk + (size_t)rr * D;
                     for (int jj = rr; jj < nj; jj += rpb, ap += (size_t)rpb * D) {
-                        const double dy = __dsub_rn(
-                            __dadd_rn(oy, __dmul_rn((double)(jb + jj), res)), bi.y);
-                        const double d2 = __dadd_rn(__dadd_rn(dx2, __dmul_rn(dy, dy)), dz2);
-                        if (d2 <= bi.r2) {
+                        const float jf = (float)(jr0 + jj);
+                        const float dyf = fmaf(jf, resf, S0.x) + fmaf(jf, resl, S0.y);
+                        const float d2f = fmaf(dyf, dyf, b2f);
+                        bool in = d2f <= lo2;
+                        if (!in && d2f <= hi2) {
+                            const BinItem bi = A.bsorted[S3.z];
+                            const int4 bx = *reinterpret_cast<const int4 *>(&A.sorted[S3.z].ibox);
+                            const double dxd =
+                                __dsub_rn(__dadd_rn(ox, __dmul_rn((double)i, res)), bi.x);
+                            const double dz = __dsub_rn(
+                                __dadd_rn(oz, __dmul_rn((double)(box_lo(bx.z) + kr0 + kk), res)), bi.z);
+                            const double dy = __dsub_rn(
+                                __dadd_rn(oy, __dmul_rn((double)(box_lo(bx.y) + jr0 + jj), res)), bi.y);
+                            const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dxd, dxd), __dmul_rn(dy, dy)),
+                                                        __dmul_rn(dz, dz));
+                            in = d2 <= bi.r2;
+                        }
+                        if (in) {
                             if (VECTOR) *ap = fmaxf(*ap, w);
                             else *ap = 1.0f;
                         }

@@ -354,3 +354,34 @@ def test_channels_whose_items_all_miss_the_grid(vector, res, dim):
                                  rng=np.random.default_rng(2))
     assert_close(np.concatenate([c for ex in got for (c, _) in ex]), np.concatenate(cgs),
                  what="far-set backward")
+
+
+@pytest.mark.parametrize("vector", [False, True])
+def test_binary_boundary_voxels_bit_exact(vector):
+    """Binary occupancy where many voxels sit exactly on (or an ulp from) the
+    sphere: atoms on voxel centers with r^2 = k res^2 (k = 1..6), and PDB-like
+    offsets -- the f32 fast test must defer every such voxel to the exact f64
+    expression."""
+    from paper_1912_04822_b200 import CoordinateSet, Example, GridMaker
+
+    res = 0.5
+    rng = np.random.default_rng(51)
+    sets = []
+    for k in range(1, 7):
+        n = 20
+        ijk = rng.integers(4, 20, size=(n, 3)).astype(np.float64)
+        coords = (-5.75 + res * ijk + np.array([41.37, -27.91, 63.05])).astype(np.float32)
+        radii = np.full(n, np.sqrt(k) * res, np.float32)
+        if vector:
+            tv = (rng.random((n, 3)) < 0.6).astype(np.float32) * rng.random((n, 3)).astype(np.float32)
+            sets.append(CoordinateSet(coords=coords, radii=radii, num_types=3, type_vector=tv))
+        else:
+            sets.append(CoordinateSet(coords=coords, radii=radii, num_types=3,
+                                      type_index=rng.integers(0, 3, n)))
+    exs = [Example(coord_sets=[s], labels=[0.0]) for s in sets]
+    center = np.array([41.37, -27.91, 63.05])
+    gm = GridMaker(resolution=res, dimension=11.5, binary=True)
+    grid = gm.forward_batch(exs, centers=np.tile(center, (len(exs), 1)))
+    go = oracle.GridOracle(resolution=res, dimension=11.5, binary=True)
+    ref = go.forward_batch(exs, centers=np.tile(center, (len(exs), 1)))
+    np.testing.assert_array_equal(grid, ref)
