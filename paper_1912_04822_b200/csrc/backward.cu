@@ -185,6 +185,9 @@ constexpr int kBwdWarps = GM_BWD_WARPS;
 #ifndef GM_BWD_F2F
 #define GM_BWD_F2F 1  // widen grid gradients with F2F (XU) instead of integer ops
 #endif
+#ifndef GM_BWDV_PTR
+#define GM_BWDV_PTR 1  // vector walk: stepped 64-bit channel pointers (vs 32-bit offsets)
+#endif
 #ifndef GM_BWDV_MINB
 #define GM_BWDV_MINB 16  // vector-mode backward: resident one-warp CTAs per SM
 #endif
@@ -521,6 +524,7 @@ __device__ __forceinline__ void vector_shared_walk(const BwdArgs &P, WarpBwd &W,
     const double qa = P.eg * (q0 * q0);
     const double m4inv_r2 = -4.0 / (r * r);
     const unsigned D3 = (unsigned)D * D * D;
+    const size_t D3l = D3;
     double tg[NC];
 #pragma unroll
     for (int c = 0; c < NC; c++) tg[c] = 0.0;
@@ -546,10 +550,18 @@ __device__ __forceinline__ void vector_shared_walk(const BwdArgs &P, WarpBwd &W,
                                     sod = (2.0 * qa) * t * rd;
                                 }
                                 float gc[NC];
+#if GM_BWDV_PTR
+                                // one 64-bit pointer stepped by the channel stride
+                                const float *gp = gset + voff;
+#pragma unroll
+                                for (int c = 0; c < NC; c++, gp += D3l)
+                                    gc[c] = (NT > 0 || c < Tn) ? __ldg(gp) : 0.0f;
+#else
                                 unsigned off = (unsigned)voff;
 #pragma unroll
                                 for (int c = 0; c < NC; c++, off += D3)
                                     gc[c] = (NT > 0 || c < Tn) ? __ldg(gset + off) : 0.0f;
+#endif
                                 double sw = 0.0;
 #pragma unroll
                                 for (int c = 0; c < NC; c++) {
