@@ -362,6 +362,9 @@ struct WarpIdx {
 };
 
 __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(const BwdArgs P) {
+    // the next prepare pass may launch now: it waits for this grid before
+    // writing the workspace this kernel reads
+    pdl_trigger();
     __shared__ WarpIdx wsm[kBwdWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int rec = blockIdx.x * kBwdWarps + warp;  // record slot (launch order)

@@ -301,6 +301,10 @@ __device__ __forceinline__ void build_slot(const PrepArgs &A, const CallArgs<CAP
 
 template <int CAP>
 __global__ void __launch_bounds__(GM_PREP_THREADS) k_prepare_static(const PrepArgs A, const __grid_constant__ CallArgs<CAP> K) {
+    // PDL: the previous kernel (a backward reading this workspace) must be
+    // done before anything is written; then the forward may launch
+    pdl_wait();
+    pdl_trigger();
     const gm_batch &b = A.b;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int nex = K.nex;
@@ -337,7 +341,8 @@ gm_status launch_static(const PrepArgs &A, const double *origins, const double *
     const int n = std::max(std::max(A.b.nitems, A.b.natoms),
                            std::max(3 * nex, nex * (A.b.nchannels + 1)));
     if (n > 0) {
-        k_prepare_static<CAP><<<(n + GM_PREP_THREADS - 1) / GM_PREP_THREADS, GM_PREP_THREADS, 0, s>>>(A, K);
+        CUDA_TRY(gm_launch_pdl(k_prepare_static<CAP>, dim3((n + GM_PREP_THREADS - 1) / GM_PREP_THREADS),
+                               dim3(GM_PREP_THREADS), 0, s, A, K));
         LAUNCH_CHECK();
     }
     return use_plane_sort(&A.p, &A.b) ? sort_planes(A, s) : GM_OK;
@@ -481,6 +486,8 @@ __global__ void __launch_bounds__(1024) k_prepare_example(const PrepArgs A) {
 
 template <bool SEGS>
 __global__ void __launch_bounds__(kSortThreads) k_sort_planes(const PrepArgs A) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int tab[(kSortMax / 32) * (kBuckets + 1)];  // chunk x bucket prefix
     __shared__ int off[kBuckets + 2];
     __shared__ int wmax_s;
@@ -607,9 +614,10 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_planes(const PrepArgs A) 
 gm_status sort_planes(const PrepArgs &A, cudaStream_t s) {
     const int nseg = A.b.nexamples * A.b.nchannels;
     if (A.b.segs) {
-        if (A.b.nsegs > 0) k_sort_planes<true><<<A.b.nsegs, kSortThreads, 0, s>>>(A);
+        if (A.b.nsegs > 0)
+            CUDA_TRY(gm_launch_pdl(k_sort_planes<true>, dim3(A.b.nsegs), dim3(kSortThreads), 0, s, A));
     } else if (nseg > 0) {
-        k_sort_planes<false><<<nseg, kSortThreads, 0, s>>>(A);
+        CUDA_TRY(gm_launch_pdl(k_sort_planes<false>, dim3(nseg), dim3(kSortThreads), 0, s, A));
     }
     LAUNCH_CHECK();
     return GM_OK;
