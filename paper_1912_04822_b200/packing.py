@@ -410,6 +410,19 @@ def _bwd_slots(coords, atom_example, example_sets, per_example=False):
         alt[0::2] = order[:(n + 1) // 2]
         alt[1::2] = order[(n + 1) // 2:][::-1]
         order = alt
+    elif _BWD_ORDER.startswith("mix:") and not per_example:
+        # H atoms from the heavy end, then L from the light end, repeated
+        h, l_ = (int(v) for v in _BWD_ORDER[4:].split(":"))
+        out, lo, hi, k = [], 0, n, 0
+        while lo < hi:
+            if k % (h + l_) < h:
+                out.append(order[lo])
+                lo += 1
+            else:
+                hi -= 1
+                out.append(order[hi])
+            k += 1
+        order = np.asarray(out, np.int64)
     slot = np.empty(n, np.int32)
     slot[order] = np.arange(n, dtype=np.int32)
     return slot
