@@ -1,3 +1,4 @@
+"""Forward with and without the job table must agree bitwise (quick GPU check)."""
 import sys, os
 sys.path.insert(0, "/root/repo")
 import numpy as np, torch
