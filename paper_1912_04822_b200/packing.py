@@ -86,6 +86,9 @@ class PackedBatch:
             atom_set[a0:a1] = s
 
         self.atom_example = set_example[atom_set] if self.natoms else np.zeros(0, np.int32)
+        # voxelizer.py:305-309 defaults (also the backward's launch-order proxy)
+        self.default_centers = np.stack([_default_center(sets) for sets in example_sets]) \
+            if self.nexamples else np.zeros((0, 3))
 
         L = _Layout()
         L.add("coords32", coords)
@@ -107,8 +110,7 @@ class PackedBatch:
                     atom_type[a0:a1] = cs.type_index
                 self.placed.append((e, choff, cs, int(a0), -1))
             L.add("atom_type", atom_type)
-            slot = _bwd_slots(coords, set_example[atom_set] if self.natoms else atom_set,
-                              example_sets)
+            slot = _bwd_slots(coords, self.atom_example, self.default_centers)
             self._bwd_slot_host = slot
             if slot is not None:
                 L.add("bwd_slot", slot)
@@ -167,8 +169,8 @@ class PackedBatch:
             L.add("item_radius", cat(it_r, np.float64))
             self.nitems = int(ipos)
             self.nweights = int(wpos)
-            slot = _bwd_slots(coords, set_example[atom_set] if self.natoms else atom_set,
-                              example_sets, per_example=True)
+            slot = _bwd_slots(coords, self.atom_example, self.default_centers,
+                              per_example=True)
             if slot is not None:
                 L.add("bwd_slot", slot)
             # item -> its entry of the packed weight rows (autograd weight refresh)
@@ -230,8 +232,6 @@ class PackedBatch:
                                                    max(self.nexamples, 1), self.nchannels)
         self.workspace = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
         self.workspace_bytes = int(nbytes)
-        self.default_centers = np.stack([_default_center(sets) for sets in example_sets]) \
-            if self.nexamples else np.zeros((0, 3))
         self._percall = None
         self._stage = None
         self._gm = None
@@ -389,7 +389,7 @@ assert _SLOT_DTYPE.itemsize == 48
 _BWD_ORDER = os.environ.get("GM_BWD_ORDER", "lpt")
 
 
-def _bwd_slots(coords, atom_example, example_sets, per_example=False):
+def _bwd_slots(coords, atom_example, centers, per_example=False):
     """Launch slot of each atom for the index-mode backward (gm_batch.bwd_slot).
 
     An atom's backward cost is its cutoff sphere's overlap with the grid, which
@@ -399,12 +399,17 @@ def _bwd_slots(coords, atom_example, example_sets, per_example=False):
     n = coords.shape[0]
     if n == 0 or _BWD_ORDER == "none":
         return None
-    centers = np.stack([_default_center(sets) for sets in example_sets])
-    d = np.linalg.norm(coords.astype(np.float64) - centers[atom_example], axis=1)
+    diff = coords - centers[atom_example].astype(np.float32)
+    d2 = np.einsum("ij,ij->i", diff, diff)
+    # distance in 1/16 A steps as a 16-bit key: numpy's radix sort (the order
+    # only has to rank atoms by cost, ties keep atom order)
+    key = np.minimum(np.sqrt(d2) * 16.0, 32767).astype(np.int16)
     # heaviest first; per_example keeps each example's atoms together (its
     # grid_grad slabs stay in L2: the vector backward reads every channel)
     per_example = per_example or _BWD_ORDER == "lpt_local"
-    order = np.lexsort((d, atom_example)) if per_example else np.argsort(d, kind="stable")
+    if per_example:
+        key = atom_example.astype(np.int64) * 32768 + key
+    order = np.argsort(key, kind="stable")
     if _BWD_ORDER == "alt":
         alt = np.empty(n, np.int64)
         alt[0::2] = order[:(n + 1) // 2]
