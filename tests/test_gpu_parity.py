@@ -385,3 +385,21 @@ def test_binary_boundary_voxels_bit_exact(vector):
     go = oracle.GridOracle(resolution=res, dimension=11.5, binary=True)
     ref = go.forward_batch(exs, centers=np.tile(center, (len(exs), 1)))
     np.testing.assert_array_equal(grid, ref)
+
+
+def test_plane_sort_fallback_for_crowded_channels():
+    """More items in one channel than the plane sort stages (1024): that
+    channel keeps item order and scans its whole range; results match."""
+    from paper_1912_04822_b200 import CoordinateSet, Example, GridMaker
+
+    rng = np.random.default_rng(61)
+    n = 1500
+    coords = rng.uniform(-6, 6, size=(n, 3)).astype(np.float32)
+    cs = CoordinateSet(coords=coords, radii=np.full(n, 1.2, np.float32), num_types=3,
+                       type_index=np.where(np.arange(n) < 1300, 0, rng.integers(1, 3, n)))
+    exs = [Example(coord_sets=[cs], labels=[0.0])]
+    gm = GridMaker(resolution=0.125, dimension=11.875)  # D = 96: plane sort enabled
+    grid = gm.forward_batch(exs, random_rotation=True, rng=np.random.default_rng(3))
+    go = oracle.GridOracle(resolution=0.125, dimension=11.875)
+    ref = go.forward_batch(exs, random_rotation=True, rng=np.random.default_rng(3))
+    assert_close(grid, ref, what="crowded channel, fine grid")
