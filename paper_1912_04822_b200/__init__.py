@@ -12,6 +12,7 @@ from .errors import ConfigError, DeviceError, FormatError, VoxmolError
 from .export import read_npy, write_npy
 from .geom import (IDENTITY_QUATERNION, Quaternion, Transform, draw_transforms,
                    make_transform, random_unit_quaternion, transform_example)
+from .graph import GraphStep
 from .voxelizer import (GridMaker, channel_count, channel_names, get_num_threads, save_grid,
                         set_num_threads)
 
@@ -21,5 +22,5 @@ __all__ = [
     "CoordinateSet", "Example", "make_vector_types", "ConfigError", "DeviceError",
     "VoxmolError", "FormatError", "read_npy", "write_npy", "IDENTITY_QUATERNION", "Quaternion", "Transform", "draw_transforms",
     "make_transform", "random_unit_quaternion", "transform_example", "GridMaker",
-    "channel_count", "channel_names", "save_grid", "set_num_threads", "get_num_threads",
+    "channel_count", "channel_names", "save_grid", "set_num_threads", "get_num_threads", "GraphStep",
 ]

@@ -7,12 +7,16 @@
 //                      forward CTA reads only its channel's items, in order
 //   k_prepare_static   batches packed with a static grouping (gm_batch.item_perm):
 //                      the same records in one fully parallel pass, per-call
-//                      arrays inside the launch
+//                      arrays inside the launch (gm_prepare_inline) or read
+//                      from the batch's device buffers (gm_prepare, graphs)
 //   k_prepare_atoms    positions only (backward without a forward)
 #include <string.h>
 
 #include "common.cuh"
 
+#ifndef GM_PREP_STATIC_DEV
+#define GM_PREP_STATIC_DEV 1  // gm_prepare on a statically grouped batch: k_prepare_static<DEV>
+#endif
 #ifndef GM_PREP_THREADS
 #define GM_PREP_THREADS 64  // small blocks: the ~50k item threads spread over every SM
 #endif
@@ -217,18 +221,18 @@ struct CallArgs {
 // Everything the prepare pass does for grouped slot t (static grouping):
 // transform (geom.py:105), forward record + binary record (returned), and in
 // index mode the position and the backward record (stored).
-template <int CAP>
-__device__ __forceinline__ void build_slot(const PrepArgs &A, const CallArgs<CAP> &K, int t,
-                                           FwdItem &f, BinItem &bi) {
+// org: the call's origins (nex,3); xf: its transforms (nex,15) or null --
+// launch parameters (inline path) or the batch's device buffers.
+__device__ __forceinline__ void build_slot(const PrepArgs &A, const double *org,
+                                           const double *xf, int t, FwdItem &f, BinItem &bi) {
     const gm_batch &b = A.b;
-    const int nex = K.nex;
     const bool vector = b.item_atom != nullptr;
     if (!vector && b.slot_rec) {
         const SlotRec R = reinterpret_cast<const SlotRec *>(b.slot_rec)[t];
         const gm_params &p = A.p;
         const int D = p.npts, e = R.ex, a = R.atom;
-        const double *X = K.has_xf ? K.v + 3 * nex + 15 * e : nullptr;
-        const double *O = K.v + 3 * e;
+        const double *X = xf ? xf + 15 * e : nullptr;
+        const double *O = org + 3 * e;
         double x[3] = {(double)R.x, (double)R.y, (double)R.z};
         if (X) {  // geom.py:105 in numpy's FMA order
             const double d[3] = {__dsub_rn(x[0], X[9]), __dsub_rn(x[1], X[10]),
@@ -291,15 +295,18 @@ __device__ __forceinline__ void build_slot(const PrepArgs &A, const CallArgs<CAP
         const int s = b.atom_set[a];
         const int e = b.set_example[s];
         double x[3];
-        transform_atom_x(A, a, s, K.has_xf ? K.v + 3 * nex + 15 * e : nullptr, x);
+        transform_atom_x(A, a, s, xf ? xf + 15 * e : nullptr, x);
         if (!vector) store_pos(A, a, x);
-        if (make_item_o(A, it, a, s, K.v + 3 * e, x, f, bi) < 0) f.ibox = 0x7fff;  // empty
-        if (!vector) store_bwd_atom(A, a, e, f.ch, K.v + 3 * e, x, f);
+        if (make_item_o(A, it, a, s, org + 3 * e, x, f, bi) < 0) f.ibox = 0x7fff;  // empty
+        if (!vector) store_bwd_atom(A, a, e, f.ch, org + 3 * e, x, f);
     }
 }
 
 
-template <int CAP>
+// DEV: the call's origins / transforms are already in the batch's device
+// buffers (b.origins / b.xforms: gm_prepare, CUDA-graph replays); otherwise
+// they travel in K and the origins are copied out for forward / backward.
+template <int CAP, bool DEV>
 __global__ void __launch_bounds__(GM_PREP_THREADS) k_prepare_static(const PrepArgs A, const __grid_constant__ CallArgs<CAP> K) {
     // PDL: the previous kernel (a backward reading this workspace) must be
     // done before anything is written; then the forward may launch
@@ -307,22 +314,24 @@ __global__ void __launch_bounds__(GM_PREP_THREADS) k_prepare_static(const PrepAr
     pdl_trigger();
     const gm_batch &b = A.b;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const int nex = K.nex;
+    const int nex = b.nexamples;
     const bool vector = b.item_atom != nullptr;
-    if (t < 3 * nex) const_cast<double *>(b.origins)[t] = K.v[t];  // for forward / backward
+    const double *org = DEV ? b.origins : K.v;
+    const double *xf = DEV ? b.xforms : (K.has_xf ? K.v + 3 * nex : nullptr);
+    if (!DEV && t < 3 * nex) const_cast<double *>(b.origins)[t] = K.v[t];  // for forward / backward
     if (t < nex * (b.nchannels + 1)) A.ws.chan_off[t] = b.chan_off[t];
     if (vector && t < b.natoms) {  // positions of all atoms
         const int s = b.atom_set[t];
         const int e = b.set_example[s];
         double x[3];
-        transform_atom_x(A, t, s, K.has_xf ? K.v + 3 * nex + 15 * e : nullptr, x);
+        transform_atom_x(A, t, s, xf ? xf + 15 * e : nullptr, x);
         store_pos(A, t, x);
         if (b.bwd_slot) A.ws.atom_order[b.bwd_slot[t]] = t;  // vector backward launch order
     }
     if (t < b.nitems) {
         FwdItem f;
         BinItem bi;
-        build_slot<CAP>(A, K, t, f, bi);
+        build_slot(A, org, xf, t, f, bi);
         A.ws.sorted[t] = f;
         A.ws.sbox[t] = make_int2(f.ibox, f.jbox);
         if (A.p.binary) A.ws.bsorted[t] = bi;
@@ -341,7 +350,25 @@ gm_status launch_static(const PrepArgs &A, const double *origins, const double *
     const int n = std::max(std::max(A.b.nitems, A.b.natoms),
                            std::max(3 * nex, nex * (A.b.nchannels + 1)));
     if (n > 0) {
-        CUDA_TRY(gm_launch_pdl(k_prepare_static<CAP>, dim3((n + GM_PREP_THREADS - 1) / GM_PREP_THREADS),
+        CUDA_TRY(gm_launch_pdl(k_prepare_static<CAP, false>,
+                               dim3((n + GM_PREP_THREADS - 1) / GM_PREP_THREADS),
+                               dim3(GM_PREP_THREADS), 0, s, A, K));
+        LAUNCH_CHECK();
+    }
+    return use_plane_sort(&A.p, &A.b) ? sort_planes(A, s) : GM_OK;
+}
+
+// Static grouping, per-call arrays already on the device (b.origins / b.xforms).
+static gm_status launch_static_dev(const PrepArgs &A, cudaStream_t s) {
+    CallArgs<1> K;
+    K.nex = A.b.nexamples;
+    K.has_xf = A.b.xforms != nullptr;
+    K.v[0] = 0.0;
+    const int nex = A.b.nexamples;
+    const int n = std::max(std::max(A.b.nitems, A.b.natoms), nex * (A.b.nchannels + 1));
+    if (n > 0) {
+        CUDA_TRY(gm_launch_pdl(k_prepare_static<1, true>,
+                               dim3((n + GM_PREP_THREADS - 1) / GM_PREP_THREADS),
                                dim3(GM_PREP_THREADS), 0, s, A, K));
         LAUNCH_CHECK();
     }
@@ -638,6 +665,7 @@ gm_status prepare_impl(const gm_params *p, const gm_batch *b, const Workspace &w
         }
         return GM_OK;
     }
+    if (b->item_perm && b->chan_off && GM_PREP_STATIC_DEV) return launch_static_dev(A, s);
     if (b->max_example_items < 0) return gm_fail(GM_ERR_INVALID, "max_example_items < 0");
     const size_t n = (size_t)b->max_example_items, nchunk = (n + 31) / 32;
     const size_t base = sizeof(int) * (2 * n + nchunk * b->nchannels + b->nchannels + 1);

@@ -307,6 +307,14 @@ class GridMaker:
         pb._last_params = p
         return out, transforms
 
+    def capture_step(self, pb: PackedBatch, *, augment=True, backward=False, grid_grad=None,
+                     out=None):
+        """prepare -> forward [-> backward] of ``pb`` captured as CUDA graphs
+        (``graph.GraphStep``): each ``run()`` is one input copy + one replay."""
+        from .graph import GraphStep
+        return GraphStep(self, pb, augment=augment, backward=backward, grid_grad=grid_grad,
+                         out=out)
+
     def backward_packed(self, pb: PackedBatch, grid_grad, centers=None, transforms=None,
                         reuse_prepared=False, coord_grad=None, type_grad=None, events=None):
         """Batched backward over every set of a packed batch.
