@@ -27,7 +27,6 @@ from __future__ import annotations
 
 import ctypes
 import math
-import os
 import subprocess
 from pathlib import Path
 

@@ -20,7 +20,6 @@ Additions:
 from __future__ import annotations
 
 import ctypes
-import json
 import math
 import os
 
@@ -29,7 +28,7 @@ import torch
 
 from . import _native, export, geom
 from .coordsets import coord_sets_of, is_coordinate_set
-from .errors import ConfigError, DeviceError
+from .errors import DeviceError
 from .packing import PackedBatch, stream_handle
 from .validation import check_rng, check_vector3
 
