@@ -185,6 +185,9 @@ constexpr int kBwdWarps = GM_BWD_WARPS;
 #ifndef GM_BWD_F2F
 #define GM_BWD_F2F 1  // widen grid gradients with F2F (XU) instead of integer ops
 #endif
+#ifndef GM_BWDV_D48
+#define GM_BWDV_D48 1  // vector backward specialised for 14 channels on 48^3 grids
+#endif
 #ifndef GM_BWDV_PTR
 #define GM_BWDV_PTR 1  // vector walk: stepped 64-bit channel pointers (vs 32-bit offsets)
 #endif
@@ -513,7 +516,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
 // set per voxel (type gradients, _kernels.py:296-313) and the coordinate
 // term from sum_c w_c g_c.  NT > 0: compile-time channel count (no
 // predicates, 32-bit channel offsets); NT = 0: up to kMaxT, predicated.
-template <int NT>
+template <int NT, int DC>
 __device__ __forceinline__ void vector_shared_walk(const BwdArgs &P, WarpBwd &W, Atom &A, int a,
                                                    int row, int Tn, const float *gset, int D,
                                                    double res, float inv_res, int lane,
@@ -554,11 +557,20 @@ __device__ __forceinline__ void vector_shared_walk(const BwdArgs &P, WarpBwd &W,
                                 }
                                 float gc[NC];
 #if GM_BWDV_PTR
-                                // one 64-bit pointer stepped by the channel stride
-                                const float *gp = gset + voff;
+                                if (DC > 0) {
+                                    // compile-time channel stride: one address,
+                                    // the channel offsets are load immediates
+                                    const float *gp = gset + voff;
 #pragma unroll
-                                for (int c = 0; c < NC; c++, gp += D3l)
-                                    gc[c] = (NT > 0 || c < Tn) ? __ldg(gp) : 0.0f;
+                                    for (int c = 0; c < NC; c++)
+                                        gc[c] = __ldg(gp + (size_t)c * DC * DC * DC);
+                                } else {
+                                    // one 64-bit pointer stepped by the channel stride
+                                    const float *gp = gset + voff;
+#pragma unroll
+                                    for (int c = 0; c < NC; c++, gp += D3l)
+                                        gc[c] = (NT > 0 || c < Tn) ? __ldg(gp) : 0.0f;
+                                }
 #else
                                 unsigned off = (unsigned)voff;
 #pragma unroll
@@ -619,10 +631,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWDV_MINB) k_backward_vecto
     if (!P.p.radius_type_indexed && Tn <= kMaxT) {
         // channel loops fully unrolled without predicates for the common
         // 14-type table, predicated up to kMaxT otherwise
-        if (Tn == 14)
-            vector_shared_walk<14>(P, wsm[warp], A, a, row, Tn, gset, D, res, inv_res, lane, gx, gy, gz);
+        if (Tn == 14 && D == 48 && GM_BWDV_D48)  // the default 0.5 A / 23.5 A grid
+            vector_shared_walk<14, 48>(P, wsm[warp], A, a, row, Tn, gset, D, res, inv_res, lane, gx, gy, gz);
+        else if (Tn == 14)
+            vector_shared_walk<14, 0>(P, wsm[warp], A, a, row, Tn, gset, D, res, inv_res, lane, gx, gy, gz);
         else
-            vector_shared_walk<0>(P, wsm[warp], A, a, row, Tn, gset, D, res, inv_res, lane, gx, gy, gz);
+            vector_shared_walk<0, 0>(P, wsm[warp], A, a, row, Tn, gset, D, res, inv_res, lane, gx, gy, gz);
     } else {
         for (int c = 0; c < Tn; c++) {
             const double r = P.p.radius_type_indexed ? b.type_radius[b.set_trstart[s] + c]
