@@ -18,6 +18,8 @@
 //    chains per lane, then a warp-shuffle reduction: no atomics, deterministic.
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace {
@@ -184,6 +186,9 @@ constexpr int kBwdWarps = GM_BWD_WARPS;
 #endif
 #ifndef GM_BWD_F2F
 #define GM_BWD_F2F 1  // widen grid gradients with F2F (XU) instead of integer ops
+#endif
+#ifndef GM_BWD_TAIL
+#define GM_BWD_TAIL 1  // index backward: single-window steps for the tail of each chunk
 #endif
 #ifndef GM_BWDV_D48
 #define GM_BWDV_D48 1  // vector backward specialised for 14 channels on 48^3 grids
@@ -468,6 +473,53 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
                         pdl_wait();
                         int cur = -1;  // rows started before the next window, minus one
                         const int last = total - 1;
+#if GM_BWD_TAIL
+                        // U windows from base; the loop's tail runs one window
+                        // at a time (no clamped dead windows).  Lane l still
+                        // visits voxels l, l+32, ... in order: same sums.
+                        auto step = [&](auto Uc, int base) {
+                            constexpr int U = decltype(Uc)::value;
+                            int myrow[U];
+#pragma unroll
+                            for (int u = 0; u < U; u++) {
+                                const unsigned M = W.starts[(base >> 5) + u];
+                                myrow[u] = cur + __popc(M & le);
+                                cur += __popc(M);
+                            }
+                            float g[U];
+#pragma unroll
+                            for (int u = 0; u < U; u++) {
+                                const int v = min(base + 32 * u + lane, last);
+                                g[u] = __ldg(W.rows[myrow[u]].gp + v);
+                            }
+#pragma unroll
+                            for (int u = 0; u < U; u++) {
+                                const int vr = base + 32 * u + lane;
+                                const int v = min(vr, last);
+                                const IRow &R = W.rows[myrow[u]];
+                                const double2 zt = W.zt[R.kz + v];
+                                const double dz = zt.x;
+                                const double d2 = fma(dz, dz, R.b2);
+                                const double rd = rsqrt_d(d2);
+                                // slope/d (_kernels.py:244-251): Gaussian core
+                                // Ex Ey Ez (-4/r^2), tail 2 qa (d - dzr) / d; d2 = 0
+                                // takes the core branch and contributes 0 (dx=dy=dz=0)
+                                const double t = d2 <= d02 ? R.exy * zt.y : fma(-qa2dzr, rd, qa2);
+#if GM_BWD_F2F
+                                const double scl = (double)((vr <= last && d2 < dzr2) ? g[u] : 0.0f) * t;
+#else
+                                const double scl = widen_if(g[u], vr <= last && d2 < dzr2) * t;
+#endif
+                                gx = fma(scl, R.dx, gx);
+                                gy = fma(scl, R.dy, gy);
+                                gz = fma(scl, dz, gz);
+                            }
+                        };
+                        int base = 0;
+                        for (; base + 32 * kU <= total; base += 32 * kU)
+                            step(std::integral_constant<int, kU>{}, base);
+                        for (; base < total; base += 32) step(std::integral_constant<int, 1>{}, base);
+#else
                         for (int base = 0; base < total; base += 32 * kU) {
                             int myrow[kU];
 #pragma unroll
@@ -505,6 +557,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
                                 gz = fma(scl, dz, gz);
                             }
                         }
+#endif
                         __syncwarp();
                     }
                 }
