@@ -148,6 +148,12 @@ __device__ __forceinline__ bool set_radius(Atom &A, double r, double rmult, doub
 
 __device__ __forceinline__ void store_coord(const BwdArgs &P, int a, int lane, double gx,
                                             double gy, double gz) {
+#if GM_BWD_SPLITSUM
+    double v[4] = {gx, gy, gz, 0.0};
+    int idx;
+    const double s = warp_sum_split<4>(v, lane, idx);  // lanes 8 idx .. 8 idx + 7
+    if ((lane & 7) == 0 && idx < 3) P.coord_grad[3 * a + idx] = (float)s;
+#else
     gx = warp_sum(gx);
     gy = warp_sum(gy);
     gz = warp_sum(gz);
@@ -156,6 +162,7 @@ __device__ __forceinline__ void store_coord(const BwdArgs &P, int a, int lane, d
         P.coord_grad[3 * a + 1] = (float)gy;
         P.coord_grad[3 * a + 2] = (float)gz;
     }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -186,6 +193,9 @@ constexpr int kBwdWarps = GM_BWD_WARPS;
 #endif
 #ifndef GM_BWD_F2F
 #define GM_BWD_F2F 1  // widen grid gradients with F2F (XU) instead of integer ops
+#endif
+#ifndef GM_BWD_SPLITSUM
+#define GM_BWD_SPLITSUM 1  // multi-value warp sums for the per-atom gradient epilogues
 #endif
 #ifndef GM_BWD_TAIL
 #define GM_BWD_TAIL 1  // index backward: single-window steps for the tail of each chunk
@@ -647,6 +657,15 @@ __device__ __forceinline__ void vector_shared_walk(const BwdArgs &P, WarpBwd &W,
                                 }
                             });
     }
+#if GM_BWD_SPLITSUM
+    static_assert(NC <= 16, "type gradients: at most 16 channels per split sum");
+    double v[16];
+#pragma unroll
+    for (int c = 0; c < 16; c++) v[c] = (c < NC && (NT > 0 || c < Tn)) ? tg[c] : 0.0;
+    int idx;
+    const double sum = warp_sum_split<16>(v, lane, idx);  // lanes 2 idx, 2 idx + 1
+    if ((lane & 1) == 0 && idx < Tn && P.type_grad) P.type_grad[row + idx] = (float)sum;
+#else
 #pragma unroll
     for (int c = 0; c < NC; c++) {
         if (NT > 0 || c < Tn) {
@@ -654,6 +673,7 @@ __device__ __forceinline__ void vector_shared_walk(const BwdArgs &P, WarpBwd &W,
             if (lane == 0 && P.type_grad) P.type_grad[row + c] = (float)v;
         }
     }
+#endif
 }
 
 // Vector types (_kernels.py:258-314).  With per-atom radii and <= kMaxT

@@ -205,6 +205,33 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// Warp sums of N2 values at once (N2 a power of two <= 32): each butterfly
+// level first halves the values a lane carries -- the lane keeps one half,
+// sends the other to its partner -- so the whole reduction moves
+// N2 - 1 + 5 - log2(N2) values instead of 5 N2.  Returns the full sum of
+// value `idx`; every lane of the idx group holds the same bits.
+template <int N2>
+__device__ __forceinline__ double warp_sum_split(double (&v)[N2], int lane, int &idx) {
+    static_assert(N2 >= 1 && N2 <= 32 && (N2 & (N2 - 1)) == 0, "N2: power of two <= 32");
+    idx = 0;
+    int o = 16;
+#pragma unroll
+    for (int h = N2 / 2; h >= 1; h >>= 1, o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int k = 0; k < h; k++) {
+            const double send = up ? v[k] : v[h + k];
+            const double keep = up ? v[h + k] : v[k];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+        if (up) idx += h;
+    }
+    double s = v[0];
+#pragma unroll
+    for (; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
 // floor(a / b) for 0 <= a < 64, 1 <= b <= 64 without an integer divide:
 // (a + 0.5) / b is at least 1/128 away from an integer.
 __device__ __forceinline__ int small_div(int a, float inv_b) {
