@@ -119,6 +119,9 @@ typedef struct {
      * instead of one per (example, channel). */
     const int32_t *segs;
     int32_t nsegs;
+    /* optional: the largest item count of any (example, channel) group, or 0 =
+     * unknown.  Sizes the plane sort's CTAs (small groups: small CTAs, one wave). */
+    int32_t max_seg_items;
 } gm_batch;
 
 /* Device scratch needed by gm_prepare / gm_forward / gm_backward. */

@@ -59,6 +59,7 @@ class GmBatch(ctypes.Structure):
         ("item_perm", _vp), ("chan_off", _vp),
         ("fwd_jobs", _vp), ("nfwd_jobs", _c_int32), ("fwd_jobs_npts", _c_int32),
         ("bwd_slot", _vp), ("slot_rec", _vp), ("segs", _vp), ("nsegs", _c_int32),
+        ("max_seg_items", _c_int32),
     ]
 
 

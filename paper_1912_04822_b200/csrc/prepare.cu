@@ -17,6 +17,9 @@
 #ifndef GM_PREP_STATIC_DEV
 #define GM_PREP_STATIC_DEV 1  // gm_prepare on a statically grouped batch: k_prepare_static<DEV>
 #endif
+#ifndef GM_SORT_SIZED
+#define GM_SORT_SIZED 1  // plane-sort CTA size from gm_batch.max_seg_items
+#endif
 #ifndef GM_PREP_THREADS
 #define GM_PREP_THREADS 64  // small blocks: the ~50k item threads spread over every SM
 #endif
@@ -25,7 +28,7 @@ struct PrepArgs;
 gm_status sort_planes(const PrepArgs &A, cudaStream_t s);
 
 // per-channel plane sort (k_sort_planes, k_prepare_seg)
-constexpr int kSortThreads = 256;
+constexpr int kSortThreads = 256;  // the largest variant
 constexpr int kSortRounds = 4;
 constexpr int kSortMax = kSortThreads * kSortRounds;  // items per channel sorted in smem
 
@@ -511,8 +514,9 @@ __global__ void __launch_bounds__(1024) k_prepare_example(const PrepArgs A) {
 // shared memory; the order is (bucket, item order): deterministic.
 // ---------------------------------------------------------------------------
 
-template <bool SEGS>
-__global__ void __launch_bounds__(kSortThreads) k_sort_planes(const PrepArgs A) {
+template <bool SEGS, int NT>
+__global__ void __launch_bounds__(NT) k_sort_planes(const PrepArgs A) {
+    constexpr int kSortThreads = NT, kSortMax = NT * kSortRounds;  // this variant
     pdl_wait();
     pdl_trigger();
     __shared__ int tab[(kSortMax / 32) * (kBuckets + 1)];  // chunk x bucket prefix
@@ -528,7 +532,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_planes(const PrepArgs A) 
     int32_t *rec = A.ws.poff + (size_t)seg * kPlaneRec;
     const int tid = threadIdx.x, lane = tid & 31;
     if (n <= 0) {
-        if (tid < kPlaneRec) rec[tid] = 0;
+        for (int t = tid; t < kPlaneRec; t += kSortThreads) rec[t] = 0;
         return;
     }
     const bool binary = A.p.binary;
@@ -574,14 +578,14 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_planes(const PrepArgs A) 
     __syncthreads();
     if (sortable) {
         // per bucket: exclusive prefix over the chunks
-        if (tid <= kBuckets) {
+        for (int t = tid; t <= kBuckets; t += kSortThreads) {
             int run = 0;
             for (int k = 0; k < nchunk; k++) {
-                const int v = tab[k * (kBuckets + 1) + tid];
-                tab[k * (kBuckets + 1) + tid] = run;
+                const int v = tab[k * (kBuckets + 1) + t];
+                tab[k * (kBuckets + 1) + t] = run;
                 run += v;
             }
-            off[tid] = run;  // bucket count, scanned below
+            off[t] = run;  // bucket count, scanned below
         }
         __syncthreads();
         if (tid < 32) {
@@ -634,20 +638,31 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_planes(const PrepArgs A) 
             if (binary) A.ws.pbsorted[cs + q] = A.ws.bsorted[cs + q];
         }
     }
-    if (tid <= kBuckets + 1) rec[tid] = sortable ? off[tid] : (tid == 0 ? 0 : n);
+    for (int t = tid; t <= kBuckets + 1; t += kSortThreads)
+        rec[t] = sortable ? off[t] : (t == 0 ? 0 : n);
     if (tid == 0) rec[kBuckets + 2] = sortable ? wmax_s : D;  // unsorted: scan everything
 }
 
-gm_status sort_planes(const PrepArgs &A, cudaStream_t s) {
+template <int NT>
+static gm_status sort_planes_nt(const PrepArgs &A, cudaStream_t s) {
     const int nseg = A.b.nexamples * A.b.nchannels;
     if (A.b.segs) {
         if (A.b.nsegs > 0)
-            CUDA_TRY(gm_launch_pdl(k_sort_planes<true>, dim3(A.b.nsegs), dim3(kSortThreads), 0, s, A));
+            CUDA_TRY(gm_launch_pdl(k_sort_planes<true, NT>, dim3(A.b.nsegs), dim3(NT), 0, s, A));
     } else if (nseg > 0) {
-        CUDA_TRY(gm_launch_pdl(k_sort_planes<false>, dim3(nseg), dim3(kSortThreads), 0, s, A));
+        CUDA_TRY(gm_launch_pdl(k_sort_planes<false, NT>, dim3(nseg), dim3(NT), 0, s, A));
     }
     LAUNCH_CHECK();
     return GM_OK;
+}
+
+// The smallest CTA that sorts the largest group in shared memory (all groups
+// resident in about one wave); unknown sizes take the largest.
+gm_status sort_planes(const PrepArgs &A, cudaStream_t s) {
+    const int m = A.b.max_seg_items;
+    if (GM_SORT_SIZED && m > 0 && m <= 64 * kSortRounds) return sort_planes_nt<64>(A, s);
+    if (GM_SORT_SIZED && m > 0 && m <= 128 * kSortRounds) return sort_planes_nt<128>(A, s);
+    return sort_planes_nt<kSortThreads>(A, s);
 }
 
 gm_status prepare_impl(const gm_params *p, const gm_batch *b, const Workspace &ws,

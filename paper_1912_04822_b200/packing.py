@@ -203,6 +203,8 @@ class PackedBatch:
         segs = np.nonzero(np.diff(chan_off.reshape(self.nexamples, -1), axis=1).reshape(-1) > 0)[0] \
             if self.nexamples else np.zeros(0, np.int64)
         self.nsegs = int(segs.shape[0])
+        self.max_seg_items = int(np.diff(chan_off.reshape(self.nexamples, -1), axis=1).max()) \
+            if self.nexamples and self.nchannels else 0
         L.add("segs", segs.astype(np.int32))
         if not self.vector_mode and self.nitems:
             # index mode: per-slot records (gm_batch.slot_rec), item_perm order
@@ -362,6 +364,7 @@ class PackedBatch:
             b.nweights = self.nweights
             b.max_example_items = self.max_example_items
             b.nsegs = self.nsegs
+            b.max_seg_items = self.max_seg_items
             for name in ("coords32", "atom_radius", "atom_set", "atom_type", "set_start",
                          "set_end", "set_example", "set_choff", "set_t", "set_wstart", "weights",
                          "type_radius", "set_trstart", "item_atom", "item_channel",
