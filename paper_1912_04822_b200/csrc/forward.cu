@@ -31,6 +31,9 @@
 
 namespace {
 
+#ifndef GM_FWD_EVICT
+#define GM_FWD_EVICT 1  // L2 evict-first hint on the grid bulk stores (C2 112.6 -> 106.7 us)
+#endif
 #ifndef GM_FWD_WARPS
 #define GM_FWD_WARPS 1
 #endif
@@ -100,9 +103,18 @@ static_assert(sizeof(Slot) == 64, "Slot must be 64 bytes");
 
 __device__ __forceinline__ void bulk_store(float *gdst, const float *ssrc, uint32_t bytes) {
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(ssrc);
+#if GM_FWD_EVICT
+    // the grids stream out: an L2 evict-first policy for their lines
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                 ::"l"(gdst), "r"(s), "r"(bytes), "l"(pol)
+                 : "memory");
+#else
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s),
                  "r"(bytes)
                  : "memory");
+#endif
 }
 
 // Ex2 / sqrt on the MUFU unit (no denormal / special-case paths: arguments
