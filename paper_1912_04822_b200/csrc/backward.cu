@@ -194,6 +194,9 @@ constexpr int kBwdWarps = GM_BWD_WARPS;
 #ifndef GM_BWD_F2F
 #define GM_BWD_F2F 1  // widen grid gradients with F2F (XU) instead of integer ops
 #endif
+#ifndef GM_BWD_PREFETCH
+#define GM_BWD_PREFETCH 1  // L2 prefetch of each row span in phase 1 (C5 438 -> 424 us)
+#endif
 #ifndef GM_BWD_GGHINT
 #define GM_BWD_GGHINT 0  // cache hint of the index-mode grid_grad loads (see ld_gg)
 #endif
@@ -499,6 +502,14 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
                                 R.exy = (W.ex[ii] * W.ey[jj]) * B.m4inv_r2;
                                 R.gp = gbase + (sbase + (unsigned)((ii * D + jj) * D + klo)) - st;
                                 R.kz = klo - st;
+#if GM_BWD_PREFETCH
+                                // the row's grid_grad span into L2 now: phase 2's
+                                // loads then hit (a hint only, no ordering)
+                                const float *rp = R.gp + st;
+                                asm volatile("prefetch.global.L2 [%0];" ::"l"(rp));
+                                if ((((uintptr_t)rp) & 127u) + 4u * (unsigned)len > 128u)
+                                    asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + len - 1));
+#endif
                             }
                             nrow += __popc(m);
                             total += __shfl_sync(0xffffffffu, sc, 31);
