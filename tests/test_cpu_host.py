@@ -334,6 +334,9 @@ def test_forward_job_table_covers_every_tile_once():
         assert lib.gm_forward_jobs(ctypes.byref(p), 3, 28, co.ctypes.data, jobs.ctypes.data,
                                    cnt) == cnt
         co2 = co.reshape(3, 29)
+        # gm_batch.max_seg_items / segs: the largest group and the groups with items
+        assert pb.max_seg_items == int(np.diff(co2, axis=1).max())
+        assert pb.nsegs == int((np.diff(co2, axis=1) > 0).sum())
         nonzero = {(e, c) for e in range(3) for c in range(28) if co2[e, c + 1] > co2[e, c]}
         seen = {}
         for e, c, t, ij in jobs:
