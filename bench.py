@@ -426,6 +426,37 @@ def main():
                        "overlapping the previous step's gridding), loss 1/2|grid|^2, "
                        "coordinate gradients read back to pinned host memory"}
 
+    # the reference-shaped API a numpy user switches to: forward_batch -> host
+    # numpy grids, backward_batch over those grids; wall clock around a few
+    # steps (host packing and both 620 MB PCIe transfers included)
+    e2e_numpy = None
+    if not args.no_e2e and ws == 1:
+        import time
+
+        nrng = np.random.default_rng(99)
+
+        def numpy_step():
+            grids, xf = gm.forward_batch(exs, random_rotation=True, random_translation=2.0,
+                                         rng=nrng, return_transforms=True)
+            gm.backward_batch(exs, grids, transforms=xf)
+
+        numpy_step()
+        torch.cuda.synchronize(dev)
+        nsteps = 3
+        t0 = time.perf_counter()
+        for _ in range(nsteps):
+            numpy_step()
+        torch.cuda.synchronize(dev)
+        n_ms = (time.perf_counter() - t0) * 1000.0 / nsteps
+        nbytes = N * C * D ** 3 * 4
+        e2e_numpy = {"value": N / (n_ms / 1000.0), "unit": "grids/s", "ms_per_step": n_ms,
+                     "steps": nsteps, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                     "note": "GridMaker.forward_batch(examples, random_rotation, "
+                             "random_translation) -> numpy grids, then backward_batch(examples, "
+                             "grids, transforms) -> per-set numpy gradients: the reference's own "
+                             "call shape with pageable host buffers, host packing per call; "
+                             "wall clock"}
+
     # write-only HBM rate of this box (torch fill of the output buffer): the
     # forward is write-dominated, so its fraction of the copy peak can exceed 1
     fa, fb = ev(), ev()
@@ -473,6 +504,7 @@ def main():
                      "fill_gbs_measured": fill_gbs,
                      "frac_of_fill": achieved / fill_gbs},
         "e2e": e2e,
+        "e2e_numpy": e2e_numpy,
         "gpu_launches": launches,
         "clocks": clk,
     }

@@ -26,7 +26,7 @@ import os
 import numpy as np
 import torch
 
-from . import _native, export, geom
+from . import _native, export, geom, hostio
 from .coordsets import coord_sets_of, is_coordinate_set
 from .errors import DeviceError
 from .packing import PackedBatch, stream_handle
@@ -457,12 +457,8 @@ class GridMaker:
         if _is_tensor(arr):
             result = arr
         else:
-            host = dout.view(shape).cpu().numpy()
-            if arr is None:
-                result = host
-            else:
-                np.copyto(arr, host)
-                result = arr
+            # pinned, chunked, multi-threaded copy-out (hostio.py)
+            result = hostio.to_host(dout.view(shape), out=arr)
         return (result, xf) if want_transforms else result
 
     def backward(self, atoms, grid_grad, center=None):
@@ -497,8 +493,7 @@ class GridMaker:
         if as_tensor:
             dgg = gg.to(torch.float32).contiguous().view((1,) + expected)
         else:
-            dgg = torch.from_numpy(np.ascontiguousarray(gg, dtype=np.float32)) \
-                .to(dev).view((1,) + expected)
+            dgg = hostio.to_device(gg, dev).view((1,) + expected)
         cg, tg = self.backward_packed(pb, dgg, centers=center.reshape(1, 3))
         if vector:
             tg = tg.view(n, int(atoms.num_types))
@@ -533,7 +528,7 @@ class GridMaker:
         if as_tensor:
             dgg = gg.to(torch.float32).contiguous()
         else:
-            dgg = torch.from_numpy(np.ascontiguousarray(gg, dtype=np.float32)).to(dev)
+            dgg = hostio.to_device(gg, dev)
         cen = None if centers is None else np.asarray(centers, np.float64).reshape(-1, 3)
         cg, tg = self.backward_packed(pb, dgg, centers=cen, transforms=transforms)
         if not as_tensor:

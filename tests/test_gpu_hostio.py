@@ -1,0 +1,55 @@
+"""hostio.py: chunked pinned host <-> device copies of the numpy-facing API
+move every byte (sizes below, at and across the chunk size), into given or
+fresh arrays, and convert dtypes like np.ascontiguousarray."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("n", [0, 1, 1000, (32 << 20) // 4, (32 << 20) // 4 + 3, 3 * (8 << 20) + 5])
+def test_round_trip(n):
+    from paper_1912_04822_b200 import hostio
+
+    a = np.random.default_rng(n).standard_normal(n).astype(np.float32)
+    d = hostio.to_device(a, "cuda")
+    assert d.dtype == torch.float32 and d.shape == (n,)
+    assert torch.equal(d.cpu(), torch.from_numpy(a))
+    back = hostio.to_host(d * 2)
+    np.testing.assert_array_equal(back, a * 2)
+    out = np.full(n, -1.0, np.float32)
+    assert hostio.to_host(d, out=out) is out
+    np.testing.assert_array_equal(out, a)
+
+
+def test_dtype_conversion_and_shape():
+    from paper_1912_04822_b200 import hostio
+
+    a = np.arange(2 * 3 * 5, dtype=np.float64).reshape(2, 3, 5)[:, ::-1]  # not contiguous
+    d = hostio.to_device(a, "cuda")
+    assert d.shape == (2, 3, 5) and d.dtype == torch.float32
+    np.testing.assert_array_equal(d.cpu().numpy(), a.astype(np.float32))
+    with pytest.raises(ValueError):
+        hostio.to_host(d, out=np.empty((2, 3, 4), np.float32))
+
+
+def test_forward_batch_numpy_out_matches_device_path():
+    from paper_1912_04822_b200 import GridMaker, synthetic
+
+    gm = GridMaker()
+    exs = synthetic.batch(4, seed=41, n_receptor=300)
+    host = gm.forward_batch(exs)
+    pb = gm.pack(exs)
+    dev, _ = gm.forward_packed(pb)
+    np.testing.assert_array_equal(host, dev.cpu().numpy())
+    given = np.empty_like(host)
+    assert gm.forward_batch(exs, out=given) is given
+    np.testing.assert_array_equal(given, host)
