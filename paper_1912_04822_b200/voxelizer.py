@@ -457,8 +457,9 @@ class GridMaker:
         if _is_tensor(arr):
             result = arr
         else:
-            # pinned, chunked, multi-threaded copy-out (hostio.py)
-            result = hostio.to_host(dout.view(shape), out=arr)
+            # pooled pinned block, or chunked multi-threaded copy-out (hostio.py)
+            result = (hostio.grid_to_numpy(dout.view(shape)) if arr is None
+                      else hostio.to_host(dout.view(shape), out=arr))
         return (result, xf) if want_transforms else result
 
     def backward(self, atoms, grid_grad, center=None):

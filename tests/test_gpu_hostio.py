@@ -53,3 +53,37 @@ def test_forward_batch_numpy_out_matches_device_path():
     given = np.empty_like(host)
     assert gm.forward_batch(exs, out=given) is given
     np.testing.assert_array_equal(given, host)
+
+
+def test_pooled_results_are_not_reused_while_viewed():
+    """forward_batch results may live in lent pinned blocks: a block is reused
+    only after every array viewing it is gone."""
+    import gc
+
+    from paper_1912_04822_b200 import GridMaker, hostio, synthetic
+
+    gm = GridMaker()
+    exs = synthetic.batch(2, seed=42, n_receptor=200)
+    want = gm.forward_batch(exs).copy()
+    a = gm.forward_batch(exs)
+    view = a[1, 3]                     # keeps a's block alive
+    del a
+    gc.collect()
+    b = gm.forward_batch(exs)
+    c = gm.forward_batch(exs)          # pool exhausted for this size: fresh memory
+    for arr in (b, c):
+        np.testing.assert_array_equal(arr, want)
+    np.testing.assert_array_equal(view, want[1, 3])
+    assert hostio.is_pooled(view) and hostio.is_pooled(b)
+    b[...] = -1.0                      # caller owns it
+    np.testing.assert_array_equal(view, want[1, 3])
+    # backward from a pooled array takes the single-DMA path and agrees
+    del b
+    gc.collect()
+    p = gm.forward_batch(exs)
+    assert hostio.is_pooled(p)
+    cg_pooled = gm.backward_batch(exs, p)
+    cg_plain = gm.backward_batch(exs, np.array(want))
+    for e in range(2):
+        for (x, _), (y, _) in zip(cg_pooled[e], cg_plain[e]):
+            np.testing.assert_array_equal(x, y)
