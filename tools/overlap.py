@@ -20,7 +20,7 @@ outs = [torch.empty((pbs[0].nexamples, pbs[0].nchannels, D, D, D), device="cuda"
 gg = torch.randn_like(outs[0])
 rng = np.random.default_rng(0)
 s_f = torch.cuda.current_stream()
-s_b = torch.cuda.Stream()
+s_b = torch.cuda.Stream(priority=int(sys.argv[2]) if len(sys.argv) > 2 else 0)
 
 
 def draw():
