@@ -178,7 +178,10 @@ class _Lent:
         self.storage, self.nbytes = storage, nbytes
 
     def __del__(self):
-        _release(self.storage, self.nbytes)
+        try:
+            _release(self.storage, self.nbytes)
+        except Exception:  # interpreter shutdown: the pool is gone anyway
+            pass
 
 
 def pinned_result(shape, dtype=np.float32):
