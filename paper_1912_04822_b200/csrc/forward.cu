@@ -54,10 +54,11 @@ namespace {
                             // 14%, 96^3 loses 8% -- its store-bound tiles want the dense order)
 #endif
 // job order: GM_FWD_ALT_H jobs from the heavy end of the sorted list, then
-// GM_FWD_ALT_L from the light end (measured on C2: 1:1 116.6 us, 1:3 112.8,
-// 2:3 112.4, 1:6 127.5)
+// GM_FWD_ALT_L from the light end (measured on C2 before the evict-first
+// stores: 1:1 116.6 us, 1:3 112.8, 2:3 112.4, 1:6 127.5; with them: 1:1 110.8,
+// 1:2 106.8, 1:3 105.6, 1:4 109.9, 2:3 106.8, 2:5 105.6, 2:7 107.6)
 #ifndef GM_FWD_ALT_H
-#define GM_FWD_ALT_H 2
+#define GM_FWD_ALT_H 1
 #endif
 #ifndef GM_FWD_ALT_L
 #define GM_FWD_ALT_L 3
