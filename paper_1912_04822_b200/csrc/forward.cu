@@ -57,7 +57,8 @@ namespace {
 // job order: GM_FWD_ALT_H jobs from the heavy end of the sorted list, then
 // GM_FWD_ALT_L from the light end (measured on C2 before the evict-first
 // stores: 1:1 116.6 us, 1:3 112.8, 2:3 112.4, 1:6 127.5; with them: 1:1 110.8,
-// 1:2 106.8, 1:3 105.6, 1:4 109.9, 2:3 106.8, 2:5 105.6, 2:7 107.6)
+// 1:2 106.8, 1:3 105.6, 1:4 109.9, 2:3 106.8, 2:5 105.6, 2:7 107.6; and with
+// zero groups of 16: 1:2 106.5, 1:3 103.3, 1:4 107.6, 2:3 109.9, 2:5 104.1)
 #ifndef GM_FWD_ALT_H
 #define GM_FWD_ALT_H 1
 #endif
