@@ -190,6 +190,50 @@ def bytes_model(cfg, exs, footprint):
     return float(fwd), float(bwd), D, C
 
 
+def pair_counts(gm, exs, sample=8):
+    """(atom, voxel) pair evaluations per grid (SURVEY 8(d) compute side): voxels
+    of each item's integer box (_kernels.py:23-31 bounds, cut = radius_multiple
+    * r, or r in binary mode) and those inside the cutoff sphere, counted in the
+    untransformed frame (rotation moves the counts by well under 1%) over the
+    first `sample` examples.  Vector types count one item per nonzero weight."""
+    res = float(gm.resolution)
+    D = gm.points_per_side()
+    mult = 1.0 if gm.binary else gm.radius_multiple
+    scale = float(gm.radius_scale)
+    pts, cuts = [], []
+    for ex in exs[:sample]:
+        sets = list(ex.coord_sets)
+        nonempty = [cs for cs in sets if cs.coords.shape[0]]
+        center = (nonempty[-1].coords.astype(np.float64).mean(axis=0) if nonempty
+                  else np.zeros(3))
+        origin = center - float(gm.dimension) / 2.0
+        for cs in sets:
+            xyz = cs.coords.astype(np.float64) - origin
+            r = cs.radii.astype(np.float64) * scale
+            if cs.type_vector is not None:
+                ia, _ = np.nonzero(cs.type_vector)
+                xyz, r = xyz[ia], r[ia]
+            pts.append(xyz)
+            cuts.append(r * mult)
+    pts, cuts = np.concatenate(pts), np.concatenate(cuts)
+    lo = np.clip(np.ceil((pts - cuts[:, None]) / res), 0, None).astype(np.int64)
+    hi = np.clip(np.floor((pts + cuts[:, None]) / res), None, D - 1).astype(np.int64)
+    ext = np.maximum(hi - lo + 1, 0)
+    box = int(np.prod(ext, axis=1).sum())
+    M = int(ext.max()) if len(ext) else 0
+    inside = 0
+    step = max(1, (1 << 22) // max(M ** 3, 1))
+    for a in range(0, len(pts), step):
+        sl = slice(a, a + step)
+        idx = lo[sl][:, :, None] + np.arange(M)[None, None, :]  # (n, 3, M)
+        d = idx * res - pts[sl][:, :, None]
+        d2 = np.where(idx <= hi[sl][:, :, None], d * d, np.inf)
+        tot = (d2[:, 0, :, None, None] + d2[:, 1, None, :, None] + d2[:, 2, None, None, :])
+        inside += int((tot <= (cuts[sl] ** 2)[:, None, None, None]).sum())
+    n = min(sample, len(exs))
+    return box / n, inside / n
+
+
 def cpu_oracle_rate(cfg, exs, budget_s=12.0, threads=None):
     """Oracle fwd+bwd grids/s on this host's cores over a bounded sample."""
     import oracle
@@ -222,6 +266,16 @@ def cpu_oracle_rate(cfg, exs, budget_s=12.0, threads=None):
     oracle.set_num_threads(n0)
     med = statistics.median(times)
     return len(sample) / med, cores, len(times), med
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args, cfg):
@@ -259,7 +313,8 @@ def run_reference(args, cfg):
         "data": "synthetic", "config": {"workload": cfg["workload"] + " (CPU sample: 8 examples/step)",
                                         "batch_per_step": len(exs)},
         "cpu_baseline": {"value": val, "unit": "grids/s", "cores": cores, "kind": "port",
-                         "sample": f"{len(exs)} examples fwd+bwd per step, OpenMP over sets/atoms"},
+                         "sample": f"{len(exs)} examples fwd+bwd per step, OpenMP over sets/atoms",
+                         "cpu_model": cpu_model()},
         "e2e": {"value": val, "unit": "grids/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -323,6 +378,7 @@ def main():
     torch.cuda.synchronize(dev)
     footprint = int((out != 0).sum().item()) / N if not cfg["binary"] else 0
     fwd_b, bwd_b, D, C = bytes_model(cfg, exs, footprint)
+    pairs_box, pairs_cut = pair_counts(gm, exs)
 
     def barrier():
         if ws > 1:
@@ -501,6 +557,14 @@ def main():
                      "step_gbs": (fwd_b + bwd_b) * N / (ms / 1000.0) / 1e9,
                      "step_frac": (fwd_b + bwd_b) * N / (ms / 1000.0) / 1e9 / peak,
                      "footprint_F_per_grid": footprint,
+                     "pairs_box_per_grid": pairs_box,
+                     "pairs_cutoff_per_grid": pairs_cut,
+                     "fwd_cutoff_pairs_per_s": pairs_cut * N / (fwd_ms / 1000.0),
+                     "bwd_cutoff_pairs_per_s": pairs_cut * N / (bwd_ms / 1000.0),
+                     "pairs_note": "(atom, voxel) pairs inside each item's cutoff sphere "
+                                   "(SURVEY 8(d) compute side), counted on the host over 8 "
+                                   "examples in the untransformed frame, outside the timed "
+                                   "region",
                      "fill_gbs_measured": fill_gbs,
                      "frac_of_fill": achieved / fill_gbs},
         "e2e": e2e,
@@ -510,10 +574,15 @@ def main():
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         rate, cores, reps, med = cpu_oracle_rate(cfg, exs, args.cpu_budget)
+        rate1, _, reps1, med1 = cpu_oracle_rate(cfg, exs, min(args.cpu_budget, 6.0), threads=1)
         line["cpu_baseline"] = {"value": rate, "unit": "grids/s", "cores": cores, "kind": "port",
                                 "sample": f"8 examples of the same workload fwd+bwd, median of "
                                           f"{reps} reps ({med * 1000:.0f} ms each), C oracle "
-                                          "with OpenMP"}
+                                          "with OpenMP",
+                                "value_1thread": rate1,
+                                "sample_1thread": f"same sample, 1 thread, median of {reps1} "
+                                                  f"reps ({med1 * 1000:.0f} ms each)",
+                                "cpu_model": cpu_model()}
     if rank == 0:
         print(json.dumps(line))
     if ws > 1:
