@@ -244,7 +244,7 @@ def cpu_oracle_rate(cfg, exs, budget_s=12.0, threads=None):
     oracle.set_num_threads(cores)
     go = oracle.GridOracle(resolution=cfg["resolution"], dimension=cfg["dimension"],
                            binary=cfg["binary"])
-    sample = exs[:8]
+    sample = exs[:cpu_sample_size(cfg)]
 
     def one():
         grid = go.forward_batch(sample, random_rotation=True, random_translation=2.0,
@@ -268,6 +268,15 @@ def cpu_oracle_rate(cfg, exs, budget_s=12.0, threads=None):
     return len(sample) / med, cores, len(times), med
 
 
+def cpu_sample_size(cfg) -> int:
+    """Examples per CPU step: the whole per-GPU batch (what the reference's
+    ``cmd_bench`` times, cli.py:377-398) unless its grids exceed 2 GB of host
+    memory (C5: 50 x 99 MB), then 8."""
+    D = int(np.floor(cfg["dimension"] / cfg["resolution"] + 0.5)) + 1
+    grid_bytes = 4 * 28 * D ** 3
+    return cfg["batch"] if cfg["batch"] * grid_bytes <= 2e9 else 8
+
+
 def cpu_model() -> str:
     try:
         for ln in open("/proc/cpuinfo"):
@@ -282,7 +291,8 @@ def run_reference(args, cfg):
     ws, rank, local = dist_env()
     if rank != 0:
         return 0
-    exs, _ = make_batch(cfg, 0, n=8)
+    nsample = cpu_sample_size(cfg)
+    exs, _ = make_batch(cfg, 0, n=nsample)
     import oracle
 
     oracle.build()
@@ -310,10 +320,14 @@ def run_reference(args, cfg):
         "value": val, "unit": "grids/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000 * el / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64 (oracle) -> f32 grids",
-        "data": "synthetic", "config": {"workload": cfg["workload"] + " (CPU sample: 8 examples/step)",
-                                        "batch_per_step": len(exs)},
+        "data": "synthetic",
+        "config": {"workload": cfg["workload"] + (
+            "" if len(exs) == cfg["batch"] else f" (CPU sample: {len(exs)} examples/step)"),
+            "batch_per_step": len(exs), "same_config": len(exs) == cfg["batch"]},
         "cpu_baseline": {"value": val, "unit": "grids/s", "cores": cores, "kind": "port",
-                         "sample": f"{len(exs)} examples fwd+bwd per step, OpenMP over sets/atoms",
+                         "sample": f"{len(exs)} examples fwd+bwd per step (the full per-GPU "
+                                   "batch)" if len(exs) == cfg["batch"] else
+                                   f"{len(exs)} examples fwd+bwd per step, OpenMP over sets/atoms",
                          "cpu_model": cpu_model()},
         "e2e": {"value": val, "unit": "grids/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -576,7 +590,8 @@ def main():
         rate, cores, reps, med = cpu_oracle_rate(cfg, exs, args.cpu_budget)
         rate1, _, reps1, med1 = cpu_oracle_rate(cfg, exs, min(args.cpu_budget, 6.0), threads=1)
         line["cpu_baseline"] = {"value": rate, "unit": "grids/s", "cores": cores, "kind": "port",
-                                "sample": f"8 examples of the same workload fwd+bwd, median of "
+                                "sample": f"{cpu_sample_size(cfg)} examples of the same "
+                                          f"workload fwd+bwd, median of "
                                           f"{reps} reps ({med * 1000:.0f} ms each), C oracle "
                                           "with OpenMP",
                                 "value_1thread": rate1,

@@ -13,6 +13,7 @@ from .export import read_npy, write_npy
 from .geom import (IDENTITY_QUATERNION, Quaternion, Transform, draw_transforms,
                    make_transform, random_unit_quaternion, transform_example)
 from .graph import GraphStep
+from .grids import GridShape, GridView, OwnedGrid, copy_into, make_grid, view_over
 from .voxelizer import (GridMaker, channel_count, channel_names, get_num_threads, save_grid,
                         set_num_threads)
 
@@ -23,4 +24,5 @@ __all__ = [
     "VoxmolError", "FormatError", "read_npy", "write_npy", "IDENTITY_QUATERNION", "Quaternion", "Transform", "draw_transforms",
     "make_transform", "random_unit_quaternion", "transform_example", "GridMaker",
     "channel_count", "channel_names", "save_grid", "set_num_threads", "get_num_threads", "GraphStep",
+    "GridShape", "GridView", "OwnedGrid", "copy_into", "make_grid", "view_over",
 ]

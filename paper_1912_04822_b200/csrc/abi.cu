@@ -5,6 +5,7 @@
 #include <math.h>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -87,6 +88,29 @@ extern "C" size_t gm_workspace_bytes(int32_t natoms, int32_t nitems, int32_t nex
     return carve_workspace(nullptr, natoms, nitems, nexamples, nchannels, nullptr);
 }
 
+// Which of our kernels last wrote / read a workspace (host-side launch order).
+// k_backward_index reads its per-atom records before its PDL wait (the
+// prologue overlaps the forward's tail).  That is only safe when the launch it
+// follows cannot still be writing those records: the forward waits for the
+// prepare pass before it triggers its dependents, the prepare pass triggers
+// before its stores.  So the early prologue is allowed only when the last of
+// our launches on this workspace was a forward.
+enum WsState { WS_UNKNOWN = 0, WS_PREPARED = 1, WS_FORWARDED = 2 };
+static std::mutex g_ws_mu;
+static std::unordered_map<const void *, int> g_ws_state;
+
+static void ws_mark(const void *workspace, int state) {
+    std::lock_guard<std::mutex> lock(g_ws_mu);
+    if (g_ws_state.size() > 4096 && !g_ws_state.count(workspace)) g_ws_state.clear();
+    g_ws_state[workspace] = state;
+}
+
+static int ws_state(const void *workspace) {
+    std::lock_guard<std::mutex> lock(g_ws_mu);
+    auto it = g_ws_state.find(workspace);
+    return it == g_ws_state.end() ? WS_UNKNOWN : it->second;
+}
+
 static Workspace ws_of(const void *workspace, const gm_batch *b) {
     Workspace w;
     carve_workspace(const_cast<void *>(workspace), b->natoms, b->nitems, b->nexamples,
@@ -110,6 +134,7 @@ extern "C" gm_status gm_prepare(const gm_params *p, const gm_batch *b, void *wor
         return gm_fail(GM_ERR_INVALID, "index mode needs one item per atom");
     if (b->nitems > 0 && !b->item_channel && !b->atom_type)
         return gm_fail(GM_ERR_INVALID, "items need item_channel or atom_type");
+    ws_mark(workspace, WS_PREPARED);
     return prepare_impl(p, b, ws_of(workspace, b), (cudaStream_t)stream, true);
 }
 
@@ -129,6 +154,7 @@ extern "C" gm_status gm_prepare_inline(const gm_params *p, const gm_batch *b, vo
     if (b->nitems > 0 && !b->item_channel && !b->atom_type)
         return gm_fail(GM_ERR_INVALID, "items need item_channel or atom_type");
     cudaStream_t s = (cudaStream_t)stream;
+    ws_mark(workspace, WS_PREPARED);
     if (b->item_perm && b->chan_off && b->nexamples <= GM_INLINE_MAX_EXAMPLES)
         return prepare_inline_impl(p, b, ws_of(workspace, b), origins_host, xforms_host, s);
     // general path: stage the per-call arrays, then the per-example grouping pass
@@ -163,7 +189,11 @@ extern "C" gm_status gm_forward(const gm_params *p, const gm_batch *b, const voi
     if (b->nexamples == 0 || b->nchannels == 0) return GM_OK;
     if (!out) return gm_fail(GM_ERR_INVALID, "out is NULL");
     if (!workspace) return gm_fail(GM_ERR_INVALID, "workspace is NULL");
-    return forward_impl(p, b, ws_of(workspace, b), out, (cudaStream_t)stream);
+    bool launched = false;
+    st = forward_impl(p, b, ws_of(workspace, b), out, (cudaStream_t)stream, &launched);
+    // an empty job table launches nothing: the prepare pass may still be running
+    if (st == GM_OK && launched) ws_mark(workspace, WS_FORWARDED);
+    return st;
 }
 
 extern "C" gm_status gm_backward(const gm_params *p, const gm_batch *b, const void *workspace,
@@ -188,7 +218,8 @@ extern "C" gm_status gm_backward(const gm_params *p, const gm_batch *b, const vo
         return gm_fail(GM_ERR_INVALID, "vector backward needs weights and set_wstart");
     if (b->vector_mode && p->radius_type_indexed && (!b->type_radius || !b->set_trstart))
         return gm_fail(GM_ERR_INVALID, "radius_type_indexed needs type_radius and set_trstart");
-    return backward_impl(p, b, ws_of(workspace, b), grid_grad, coord_grad, type_grad, s);
+    const bool early = ws_state(workspace) == WS_FORWARDED;
+    return backward_impl(p, b, ws_of(workspace, b), grid_grad, coord_grad, type_grad, s, early);
 }
 
 // ----------------------------------------------------------------------------
@@ -471,8 +502,9 @@ static gm_status run_host_backward(double *coord_grad, double *type_grad, const 
     const size_t o_gg = plan.add(grid_grad, sizeof(float) * nt * D3);
     const size_t ws_bytes = gm_workspace_bytes((int32_t)n, (int32_t)n, 1, (int32_t)nt);
     const size_t o_ws = plan.add(nullptr, ws_bytes);
-    const size_t o_cg = plan.add(nullptr, sizeof(float) * 3 * n);
-    const size_t o_tg = plan.add(nullptr, sizeof(float) * (vector_mode ? n * nt : 1));
+    // f64 outputs: the numba kernels return their f64 sums (_kernels.py:214,265-266)
+    const size_t o_cg = plan.add(nullptr, sizeof(double) * 3 * n);
+    const size_t o_tg = plan.add(nullptr, sizeof(double) * (vector_mode ? n * nt : 1));
     Arena &ar = t_arena;
     CUDA_TRY(ar.buf.reserve(plan.used));
     char *d = (char *)ar.buf.ptr;
@@ -510,16 +542,13 @@ static gm_status run_host_backward(double *coord_grad, double *type_grad, const 
     // index mode: the backward reuses the forward items' boxes
     gm_status st = prepare_impl(&p, &b, ws_of(d + o_ws, &b), nullptr, !vector_mode);
     if (st) return st;
-    st = gm_backward(&p, &b, d + o_ws, (const float *)(d + o_gg), (float *)(d + o_cg),
-                               vector_mode ? (float *)(d + o_tg) : nullptr, nullptr);
+    st = backward_impl(&p, &b, ws_of(d + o_ws, &b), (const float *)(d + o_gg), nullptr, nullptr,
+                       nullptr, false, (double *)(d + o_cg),
+                       vector_mode ? (double *)(d + o_tg) : nullptr);
     if (st) return st;
-    std::vector<float> cg(3 * n), tg(vector_mode ? n * nt : 0);
-    CUDA_TRY(cudaMemcpy(cg.data(), d + o_cg, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < 3 * n; i++) coord_grad[i] = cg[i];
-    if (vector_mode) {
-        CUDA_TRY(cudaMemcpy(tg.data(), d + o_tg, sizeof(float) * n * nt, cudaMemcpyDeviceToHost));
-        for (int64_t i = 0; i < n * nt; i++) type_grad[i] = tg[i];
-    }
+    CUDA_TRY(cudaMemcpy(coord_grad, d + o_cg, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+    if (vector_mode)
+        CUDA_TRY(cudaMemcpy(type_grad, d + o_tg, sizeof(double) * n * nt, cudaMemcpyDeviceToHost));
     return GM_OK;
 }
 

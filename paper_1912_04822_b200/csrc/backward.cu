@@ -33,9 +33,13 @@ struct BwdArgs {
     const float *grid_grad;
     float *coord_grad;
     float *type_grad;
+    double *coord_grad64;  // optional f64 outputs (the reference-shaped *_host entry
+    double *type_grad64;   // points return the f64 sums like _kernels.py:214,265)
     const BwdAtom *batoms; // index mode: per-atom records of the prepare pass
     const int32_t *atom_order; // vector mode: atom of each launch slot (bwd_slot inverse)
     double eg;             // exp(-2 grm^2), a batch constant (_kernels.py:224)
+    int early;             // 1: the records may be read before the PDL wait (the
+                           // previous launch on this workspace was the forward)
 };
 
 
@@ -152,12 +156,19 @@ __device__ __forceinline__ void store_coord(const BwdArgs &P, int a, int lane, d
     double v[4] = {gx, gy, gz, 0.0};
     int idx;
     const double s = warp_sum_split<4>(v, lane, idx);  // lanes 8 idx .. 8 idx + 7
-    if ((lane & 7) == 0 && idx < 3) P.coord_grad[3 * a + idx] = (float)s;
+    if ((lane & 7) == 0 && idx < 3) {
+        if (P.coord_grad64) P.coord_grad64[3 * a + idx] = s;
+        else P.coord_grad[3 * a + idx] = (float)s;
+    }
 #else
     gx = warp_sum(gx);
     gy = warp_sum(gy);
     gz = warp_sum(gz);
-    if (lane == 0) {
+    if (lane == 0 && P.coord_grad64) {
+        P.coord_grad64[3 * a + 0] = gx;
+        P.coord_grad64[3 * a + 1] = gy;
+        P.coord_grad64[3 * a + 2] = gz;
+    } else if (lane == 0) {
         P.coord_grad[3 * a + 0] = (float)gx;
         P.coord_grad[3 * a + 1] = (float)gy;
         P.coord_grad[3 * a + 2] = (float)gz;
@@ -421,6 +432,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
     const int D = P.p.npts;
     const double res = P.p.resolution;
     const float inv_res = (float)(1.0 / res);
+    // right after a prepare pass (which triggers its dependents before its
+    // stores) the records are only valid after the wait
+    if (!P.early) pdl_wait();
     // the prepare pass's record: position relative to the origin, constants,
     // and the forward item's box (_kernels.py:225-227) -- one load level
     const BwdAtom B = P.batoms[rec];
@@ -702,13 +716,17 @@ __device__ __forceinline__ void vector_shared_walk(const BwdArgs &P, WarpBwd &W,
     for (int c = 0; c < 16; c++) v[c] = (c < NC && (NT > 0 || c < Tn)) ? tg[c] : 0.0;
     int idx;
     const double sum = warp_sum_split<16>(v, lane, idx);  // lanes 2 idx, 2 idx + 1
-    if ((lane & 1) == 0 && idx < Tn && P.type_grad) P.type_grad[row + idx] = (float)sum;
+    if ((lane & 1) == 0 && idx < Tn) {
+        if (P.type_grad64) P.type_grad64[row + idx] = sum;
+        else if (P.type_grad) P.type_grad[row + idx] = (float)sum;
+    }
 #else
 #pragma unroll
     for (int c = 0; c < NC; c++) {
         if (NT > 0 || c < Tn) {
             const double v = warp_sum(tg[c]);
-            if (lane == 0 && P.type_grad) P.type_grad[row + c] = (float)v;
+            if (lane == 0 && P.type_grad64) P.type_grad64[row + c] = v;
+            else if (lane == 0 && P.type_grad) P.type_grad[row + c] = (float)v;
         }
     }
 #endif
@@ -785,7 +803,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWDV_MINB) k_backward_vecto
                                 });
             }
             tg = warp_sum(tg);
-            if (lane == 0 && P.type_grad) P.type_grad[row + c] = (float)tg;
+            if (lane == 0 && P.type_grad64) P.type_grad64[row + c] = tg;
+            else if (lane == 0 && P.type_grad) P.type_grad[row + c] = (float)tg;
         }
     }
     store_coord(P, a, lane, gx, gy, gz);
@@ -795,8 +814,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWDV_MINB) k_backward_vecto
 
 gm_status backward_impl(const gm_params *p, const gm_batch *b, const Workspace &ws,
                         const float *grid_grad, float *coord_grad, float *type_grad,
-                        cudaStream_t s) {
+                        cudaStream_t s, bool early_prologue, double *coord_grad64,
+                        double *type_grad64) {
     BwdArgs P;
+    P.coord_grad64 = coord_grad64;
+    P.type_grad64 = type_grad64;
+    P.early = early_prologue ? 1 : 0;
     P.p = *p;
     P.b = *b;
     P.pos = ws.pos;

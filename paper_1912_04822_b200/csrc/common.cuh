@@ -249,10 +249,12 @@ gm_status prepare_impl(const gm_params *p, const gm_batch *b, const Workspace &w
                        cudaStream_t s, bool items_too);
 gm_status prepare_inline_impl(const gm_params *p, const gm_batch *b, const Workspace &ws,
                               const double *origins, const double *xforms, cudaStream_t s);
+// *launched: whether a kernel was launched (an empty job table launches none)
 gm_status forward_impl(const gm_params *p, const gm_batch *b, const Workspace &ws, float *out,
-                       cudaStream_t s);
+                       cudaStream_t s, bool *launched = nullptr);
 int32_t forward_jobs_impl(const gm_params *p, int32_t nex, int32_t nch, const int32_t *chan_off,
                           int32_t *jobs, int32_t cap);
 gm_status backward_impl(const gm_params *p, const gm_batch *b, const Workspace &ws,
                         const float *grid_grad, float *coord_grad, float *type_grad,
-                        cudaStream_t s);
+                        cudaStream_t s, bool early_prologue = false,
+                        double *coord_grad64 = nullptr, double *type_grad64 = nullptr);

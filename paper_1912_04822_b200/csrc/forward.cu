@@ -498,27 +498,31 @@ FwdConfig choose_config(int D) {
 }
 
 template <bool BIN, bool VEC, bool RESL>
-gm_status launch(const FwdArgs &A, const FwdConfig &cfg, int nex, int njobs, cudaStream_t s) {
+gm_status launch(const FwdArgs &A, const FwdConfig &cfg, int nex, int njobs, cudaStream_t s,
+                 bool *launched) {
     auto kern = k_forward<BIN, VEC, RESL>;
     CUDA_TRY(gm_ensure_smem((const void *)kern, (int)cfg.smem));
     if (A.jobs) {
         if (njobs > 0) {
             CUDA_TRY(gm_launch_pdl(kern, dim3(njobs), dim3(kThreads), cfg.smem, s, A));
+            LAUNCH_CHECK();
+            if (launched) *launched = true;
         }
-        LAUNCH_CHECK();
         return GM_OK;
     }
     if (A.ntiles > 65535 || nex > 65535) return gm_fail(GM_ERR_INVALID, "too many examples or tiles");
     dim3 grid(A.C, A.ntiles, nex);
     CUDA_TRY(gm_launch_pdl(kern, grid, dim3(kThreads), cfg.smem, s, A));
     LAUNCH_CHECK();
+    if (launched) *launched = true;
     return GM_OK;
 }
 
 }  // namespace
 
 gm_status forward_impl(const gm_params *p, const gm_batch *b, const Workspace &ws, float *out,
-                       cudaStream_t s) {
+                       cudaStream_t s, bool *launched) {
+    if (launched) *launched = false;
     const int D = p->npts;
     const FwdConfig cfg = choose_config(D);
     if (cfg.smem > 227 * 1024) return gm_fail(GM_ERR_INVALID, "grid too large for one tile row");
@@ -550,11 +554,11 @@ gm_status forward_impl(const gm_params *p, const gm_batch *b, const Workspace &w
     A.jobs = jobs ? reinterpret_cast<const int4 *>(b->fwd_jobs) : nullptr;
     const int nj = jobs ? b->nfwd_jobs : 0;
     if (p->binary)
-        return b->vector_mode ? launch<true, true, false>(A, cfg, b->nexamples, nj, s)
-                              : launch<true, false, false>(A, cfg, b->nexamples, nj, s);
+        return b->vector_mode ? launch<true, true, false>(A, cfg, b->nexamples, nj, s, launched)
+                              : launch<true, false, false>(A, cfg, b->nexamples, nj, s, launched);
     // resolutions exactly representable in f32 (0.5, 0.25, 0.375 ...) drop the lo term
-    return A.resl != 0.0f ? launch<false, false, true>(A, cfg, b->nexamples, nj, s)
-                          : launch<false, false, false>(A, cfg, b->nexamples, nj, s);
+    return A.resl != 0.0f ? launch<false, false, true>(A, cfg, b->nexamples, nj, s, launched)
+                          : launch<false, false, false>(A, cfg, b->nexamples, nj, s, launched);
 }
 
 // Job table of a static grouping: every tile of a channel with items, and the

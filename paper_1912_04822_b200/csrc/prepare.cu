@@ -237,6 +237,11 @@ __device__ __forceinline__ void build_slot(const PrepArgs &A, const double *org,
         const double *X = xf ? xf + 15 * e : nullptr;
         const double *O = org + 3 * e;
         double x[3] = {(double)R.x, (double)R.y, (double)R.z};
+        if (b.coords64) {  // positions given in f64 (host-transformed exact mode)
+            x[0] = b.coords64[3 * a + 0];
+            x[1] = b.coords64[3 * a + 1];
+            x[2] = b.coords64[3 * a + 2];
+        }
         if (X) {  // geom.py:105 in numpy's FMA order
             const double d[3] = {__dsub_rn(x[0], X[9]), __dsub_rn(x[1], X[10]),
                                  __dsub_rn(x[2], X[11])};

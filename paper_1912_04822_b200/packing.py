@@ -261,7 +261,17 @@ class PackedBatch:
         """Replace the packed input-frame coordinates with a (natoms, 3)
         device tensor (a device-to-device copy, stream-ordered)."""
         if self.natoms:
-            self.device_view("coords32").copy_(coords.detach().reshape(self.natoms, 3))
+            c = coords.detach().reshape(self.natoms, 3).to(torch.float32)
+            self.device_view("coords32").copy_(c)
+            if "slot_rec" in self.offsets:
+                # index mode: the prepare pass starts from the per-slot records
+                # (x, y, z gathered at pack time in item_perm order), so they
+                # must follow the new coordinates too
+                if getattr(self, "_perm_dev", None) is None:
+                    self._perm_dev = self.device_view("item_perm").to(torch.int64)
+                off = self.offsets["slot_rec"][0]
+                rec = self.dev[off:off + 48 * self.nitems].view(torch.float32).view(self.nitems, 12)
+                rec[:, 0:3] = c[self._perm_dev]
 
     def load_weights(self, weights: torch.Tensor) -> None:
         """Vector mode: replace the packed type weights (nweights,) and the
@@ -275,6 +285,24 @@ class PackedBatch:
             if getattr(self, "_item_windex_dev", None) is None:
                 self._item_windex_dev = torch.from_numpy(self.item_windex).to(self.device)
             self.device_view("item_weight").copy_(w[self._item_windex_dev])
+
+    def set_host_positions(self, pos: np.ndarray | None) -> None:
+        """Exact-transform fallback: (natoms, 3) float64 positions already in
+        the call's frame (gm_batch.coords64; the prepare pass then applies no
+        transform), or None to return to device-side transforms."""
+        if pos is None:
+            self._want_coords64 = False
+            if self._gm is not None:
+                self._gm.coords64 = None
+            return
+        if getattr(self, "_pos64", None) is None:
+            self._pos64 = torch.empty((max(self.natoms, 1), 3), dtype=torch.float64,
+                                      device=self.device)
+        if self.natoms:
+            self._pos64[:self.natoms].copy_(torch.from_numpy(np.ascontiguousarray(pos)))
+        self._want_coords64 = True
+        if self._gm is not None:
+            self._gm.coords64 = self._pos64.data_ptr()
 
     def ptr(self, name: str) -> int | None:
         if name not in self.offsets:
@@ -335,6 +363,18 @@ class PackedBatch:
         if _NO_JOBS or self._gm is None or getattr(self, "_jobs_npts", None) == npts or \
                 not self.nexamples or not self.nchannels:
             return
+        # one table per grid size, kept for the batch's lifetime: a captured
+        # CUDA graph (graph.GraphStep) bakes the table's pointer into its
+        # forward node, so a table must never be freed while the batch lives
+        if not hasattr(self, "_jobs_by_npts"):
+            self._jobs_by_npts = {}
+        if npts in self._jobs_by_npts:
+            self._jobs, cnt = self._jobs_by_npts[npts]
+            self._jobs_npts = npts
+            self._gm.fwd_jobs = self._jobs.data_ptr()
+            self._gm.nfwd_jobs = int(cnt)
+            self._gm.fwd_jobs_npts = npts
+            return
         off = self.offsets["chan_off"][0]
         n = self.nexamples * (self.nchannels + 1)
         co = np.ascontiguousarray(self.host.numpy()[off:off + 4 * n].view(np.int32))
@@ -347,6 +387,7 @@ class PackedBatch:
         lib.gm_forward_jobs(ctypes.byref(params), self.nexamples, self.nchannels,
                             co.ctypes.data, jobs.ctypes.data, cnt)
         self._jobs = torch.from_numpy(jobs).to(self.device)
+        self._jobs_by_npts[npts] = (self._jobs, int(cnt))
         self._jobs_npts = npts
         self._gm.fwd_jobs = self._jobs.data_ptr()
         self._gm.nfwd_jobs = int(cnt)
@@ -371,6 +412,8 @@ class PackedBatch:
                          "item_weight", "item_radius", "ex_item_start", "ex_item_end",
                          "item_perm", "chan_off", "bwd_slot", "slot_rec", "segs"):
                 setattr(b, name, self.ptr(name))
+            if getattr(self, "_want_coords64", False) and self._pos64 is not None:
+                b.coords64 = self._pos64.data_ptr()
             base = self._percall.data_ptr()
             b.origins = base
             b.xforms = base + 8 * 3 * self.nexamples if self._has_xforms else None

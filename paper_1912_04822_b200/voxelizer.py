@@ -250,6 +250,14 @@ class GridMaker:
                                    else np.asarray(t, np.float64).reshape(15)
                                    for t in transforms]) if len(transforms) else np.zeros((0, 15))
         p = self._gm_params(npts)
+        pb.set_host_positions(None)
+        if xforms is not None and (p.matmul_order_1 < 0 or p.matmul_order_n < 0):
+            # numpy's f64 (N,3)@(3,3) rounding could not be reproduced on the
+            # device: transform on the host with the
+            # reference's own expression (geom.py:105) and ship f64 positions
+            _warn_exact_fallback()
+            pb.set_host_positions(_host_transformed(pb, xforms))
+            xforms = None
         if pb.nexamples <= _native.INLINE_MAX_EXAMPLES:
             # per-call arrays travel inside the prepare launch (no copy)
             pb.ensure_call_buffer(xforms is not None)
@@ -429,20 +437,16 @@ class GridMaker:
             rng = check_rng(rng)
         vector_mode = _batch_mode(example_sets)
         if vector_mode is None:
-            # nothing but empty sets: a zero grid, but the transforms are still
-            # drawn in example order (voxelizer.py:357-363 draws before packing)
+            # nothing but empty sets: a zero grid.  The reference returns
+            # before its per-example make_transform loop (voxelizer.py:351-352),
+            # so no variate is drawn and the caller's generator is untouched.
             if arr is None:
                 arr = np.zeros(shape, dtype=np.float32)
             elif _is_tensor(arr):
                 arr.zero_()
             else:
                 arr[...] = 0.0
-            xf = None
-            if augment:
-                c = centers if centers is not None else np.stack(
-                    [_host_default_center(s) for s in example_sets])
-                xf = geom.draw_transforms(c, float(random_translation), bool(random_rotation), rng)
-            return (arr, xf) if want_transforms else arr
+            return (arr, None) if want_transforms else arr
         nch = shape[0] if single else shape[1]
         dev = arr.device if _is_tensor(arr) else self._device()
         pb = self.pack(example_sets, nchannels=nch, device=dev)
@@ -551,6 +555,36 @@ class GridMaker:
         return out
 
 
+_FALLBACK_WARNED = [False]
+
+
+def _warn_exact_fallback() -> None:
+    if not _FALLBACK_WARNED[0]:
+        import warnings
+
+        warnings.warn("numpy's float64 matmul rounding could not be calibrated on this host; "
+                      "augmented coordinates are transformed on the host (exact, slower)",
+                      RuntimeWarning, stacklevel=3)
+        _FALLBACK_WARNED[0] = True
+
+
+def _host_transformed(pb: PackedBatch, xforms) -> np.ndarray:
+    """(natoms, 3) float64 transformed coordinates, set by set, with the
+    reference's expression ((x - c) @ R.T + c) + t (geom.py:105 via
+    voxelizer.py:366-368): the same numpy matmul call per set, so the same
+    BLAS rounding whatever its FMA order."""
+    xf = np.asarray(xforms, np.float64).reshape(-1, 15)
+    pos = np.zeros((pb.natoms, 3), np.float64)
+    for (e, _choff, cs, a0, _w0) in pb.placed:
+        n = int(cs.coords.shape[0])
+        if not n:
+            continue
+        R = np.ascontiguousarray(xf[e, :9]).reshape(3, 3)
+        c, t = xf[e, 9:12], xf[e, 12:15]
+        pos[a0:a0 + n] = (cs.coords.astype(np.float64) - c) @ R.T + c + t
+    return pos
+
+
 def _rotation_of(t) -> np.ndarray:
     if isinstance(t, geom.Transform):
         return t.rotation.rotation_matrix()
@@ -572,13 +606,6 @@ def _batch_mode(example_sets):
             elif mode != vec:
                 raise ValueError("cannot mix index- and vector-typed sets in one batch")
     return mode
-
-
-def _host_default_center(sets) -> np.ndarray:
-    for cs in reversed(sets):
-        if cs.coords.shape[0]:
-            return cs.centroid()
-    return np.zeros(3, dtype=np.float64)
 
 
 def _check_device_out(t, shape, device):

@@ -263,6 +263,23 @@ def test_batch_validation_before_device():
         gm.forward(a)
 
 
+def test_all_empty_batch_consumes_no_random_numbers():
+    """voxelizer.py:351-352: a batch of empty sets returns before any
+    make_transform call, so the caller's generator is untouched."""
+    from paper_1912_04822_b200 import CoordinateSet, Example, GridMaker
+
+    empty = CoordinateSet(coords=np.zeros((0, 3), np.float32), radii=np.zeros(0, np.float32),
+                          num_types=3, type_index=np.zeros(0, np.int64))
+    gm = GridMaker(dimension=4.0)
+    rng = np.random.default_rng(42)
+    before = rng.bit_generator.state
+    grid, xf = gm.forward_batch([Example([empty]), Example([empty])], random_rotation=True,
+                                random_translation=2.0, rng=rng, return_transforms=True)
+    assert rng.bit_generator.state == before
+    assert xf is None
+    assert grid.shape == (2, 3, 9, 9, 9) and not grid.any()
+
+
 def test_packing_layout_cpu():
     import torch
 

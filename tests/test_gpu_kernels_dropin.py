@@ -89,6 +89,9 @@ def test_backward_index_dropin():
                                        go.rmult)
     assert got.dtype == np.float64 and got.shape == (coords.shape[0], 3)
     assert_close(got, want, what="backward_index")
+    # f64 sums like the numba kernel (_kernels.py:214), not f32-rounded values
+    assert_close(got, want, rel=1e-9, abs_=1e-10, what="backward_index f64")
+    assert (got != got.astype(np.float32).astype(np.float64)).any()
 
 
 @pytest.mark.parametrize("rti", [False, True])
@@ -111,3 +114,6 @@ def test_backward_vector_dropin(rti):
                                         int(rti), origin, go.resolution, go.grm, go.rmult)
     assert_close(cg, wc, what="coord")
     assert_close(tg, wt, what="type")
+    assert_close(cg, wc, rel=1e-9, abs_=1e-10, what="coord f64")
+    assert_close(tg, wt, rel=1e-9, abs_=1e-10, what="type f64")
+    assert (tg != tg.astype(np.float32).astype(np.float64)).any()
