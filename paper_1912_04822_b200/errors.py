@@ -23,3 +23,18 @@ class FormatError(VoxmolError, ValueError):
 
 class DeviceError(VoxmolError, RuntimeError):
     """The CUDA extension reported a launch or resource failure."""
+
+
+def use_exception_classes(ref_errors) -> None:
+    """Raise the reference's own exception classes from now on.
+
+    For mixed deployments where callers catch ``voxmol.errors.ConfigError``
+    / ``FormatError`` (e.g. the reference's test suite run against this
+    GridMaker, tests/refsuite_plugin.py): pass the reference's ``errors``
+    module and every raise site of this package (which looks the class up
+    in this module at raise time) uses its classes.
+    """
+    g = globals()
+    for name in ("VoxmolError", "ConfigError", "FormatError"):
+        if hasattr(ref_errors, name):
+            g[name] = getattr(ref_errors, name)

@@ -20,7 +20,7 @@ import struct
 
 import numpy as np
 
-from .errors import FormatError
+from . import errors
 
 _NPY_MAGIC = b"\x93NUMPY"
 
@@ -127,32 +127,32 @@ def read_npy(path) -> np.ndarray:
     with open(path, "rb") as fh:
         magic = fh.read(6)
         if magic != _NPY_MAGIC:
-            raise FormatError(f"{path}: not an NPY file (bad magic {magic!r})")
+            raise errors.FormatError(f"{path}: not an NPY file (bad magic {magic!r})")
         version = fh.read(2)
         if len(version) < 2 or version[0] != 1:
-            raise FormatError(f"{path}: unsupported NPY version {tuple(version)!r}")
+            raise errors.FormatError(f"{path}: unsupported NPY version {tuple(version)!r}")
         raw_len = fh.read(2)
         if len(raw_len) < 2:
-            raise FormatError(f"{path}: truncated NPY header")
+            raise errors.FormatError(f"{path}: truncated NPY header")
         (hlen,) = struct.unpack("<H", raw_len)
         header = fh.read(hlen)
         if len(header) < hlen:
-            raise FormatError(f"{path}: truncated NPY header")
+            raise errors.FormatError(f"{path}: truncated NPY header")
         try:
             meta = ast.literal_eval(header.decode("latin1"))
         except (ValueError, SyntaxError) as exc:
-            raise FormatError(f"{path}: unparseable NPY header") from exc
+            raise errors.FormatError(f"{path}: unparseable NPY header") from exc
         descr = meta.get("descr")
         if descr not in ("<f4", "<f8"):
-            raise FormatError(f"{path}: unsupported descr {descr!r}, expected <f4/<f8")
+            raise errors.FormatError(f"{path}: unsupported descr {descr!r}, expected <f4/<f8")
         if meta.get("fortran_order"):
-            raise FormatError(f"{path}: fortran-order NPY files are not supported")
+            raise errors.FormatError(f"{path}: fortran-order NPY files are not supported")
         shape = tuple(meta.get("shape", ()))
         count = int(np.prod(shape)) if shape else 1
         payload = fh.read()
     expected = count * np.dtype(descr).itemsize
     if len(payload) < expected:
-        raise FormatError(f"{path}: truncated NPY payload ({len(payload)} < {expected} bytes)")
+        raise errors.FormatError(f"{path}: truncated NPY payload ({len(payload)} < {expected} bytes)")
     return np.frombuffer(payload[:expected], dtype=descr).reshape(shape).copy()
 
 

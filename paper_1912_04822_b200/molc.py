@@ -28,7 +28,7 @@ import struct
 import numpy as np
 
 from .coordsets import CoordinateSet
-from .errors import FormatError
+from . import errors
 
 MOLC_MAGIC = b"MOLC"
 MOLC_VERSION = 1
@@ -71,7 +71,7 @@ class MolcCache:
         self._fh = open(self.path, "rb")
         try:
             if os.fstat(self._fh.fileno()).st_size < 24:
-                raise FormatError(f"{self.path}: file too small to be a MOLC cache")
+                raise errors.FormatError(f"{self.path}: file too small to be a MOLC cache")
             self._mm = mmap.mmap(self._fh.fileno(), 0, access=mmap.ACCESS_READ)
             self._buf = np.frombuffer(self._mm, dtype=np.uint8)
             self._index = self._load_index()
@@ -83,14 +83,14 @@ class MolcCache:
     def _load_index(self) -> dict:
         mm = self._mm
         if mm[:4] != MOLC_MAGIC:
-            raise FormatError(f"{self.path}: bad magic {bytes(mm[:4])!r}")
+            raise errors.FormatError(f"{self.path}: bad magic {bytes(mm[:4])!r}")
         (version,) = struct.unpack_from("<I", mm, 4)
         if version != MOLC_VERSION:
-            raise FormatError(f"{self.path}: unsupported cache version {version}")
+            raise errors.FormatError(f"{self.path}: unsupported cache version {version}")
         (count,) = struct.unpack_from("<Q", mm, 8)
         (index_offset,) = struct.unpack_from("<Q", mm, len(mm) - 8)
         if not 16 <= index_offset <= len(mm) - 8:
-            raise FormatError(f"{self.path}: index offset {index_offset} out of range")
+            raise errors.FormatError(f"{self.path}: index offset {index_offset} out of range")
         index, pos = {}, index_offset
         try:
             for _ in range(count):
@@ -99,12 +99,12 @@ class MolcCache:
                 (off,) = struct.unpack_from("<Q", mm, pos + 2 + nlen)
                 pos += 10 + nlen
                 if not 16 <= off < index_offset:
-                    raise FormatError(f"{self.path}: entry offset {off} out of range")
+                    raise errors.FormatError(f"{self.path}: entry offset {off} out of range")
                 index[name] = off
         except (struct.error, UnicodeDecodeError) as exc:
-            raise FormatError(f"{self.path}: truncated or corrupt index") from exc
+            raise errors.FormatError(f"{self.path}: truncated or corrupt index") from exc
         if pos != len(mm) - 8:
-            raise FormatError(f"{self.path}: index does not span to footer")
+            raise errors.FormatError(f"{self.path}: index does not span to footer")
         return index
 
     # -- lookups -----------------------------------------------------------
@@ -121,10 +121,10 @@ class MolcCache:
             off += 2 + nlen
             (natoms,) = struct.unpack_from("<I", self._mm, off)
         except struct.error as exc:
-            raise FormatError(f"{self.path}: truncated entry for {name!r}") from exc
+            raise errors.FormatError(f"{self.path}: truncated entry for {name!r}") from exc
         off += 4
         if off + natoms * ATOM_DTYPE.itemsize > len(self._mm):
-            raise FormatError(f"{self.path}: truncated entry for {name!r}")
+            raise errors.FormatError(f"{self.path}: truncated entry for {name!r}")
         return off, natoms
 
     def records(self, name: str) -> np.ndarray:

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .errors import ConfigError
+from . import errors
 
 _ALIGN = 256
 # GM_NO_JOBS=1: dense forward launch (A/B timing of the job table)
@@ -137,7 +137,7 @@ class PackedBatch:
                       else np.asarray(cs.type_vector, np.float32))
                 if radius_type_indexed and na:
                     if cs.type_radii is None:
-                        raise ConfigError(
+                        raise errors.ConfigError(
                             "radius_type_indexed requires coordinate sets typed from a table "
                             "(type_radii is missing)")
                     tr = cs.type_radii.astype(np.float64) * scale

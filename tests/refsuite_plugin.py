@@ -27,8 +27,11 @@ def _install():
 
     voxmol._kernels = gpu_kernels
     if mode == "gridmaker":
+        import voxmol.errors
         import voxmol.voxelizer as vz
-        from paper_1912_04822_b200 import GridMaker
+        from paper_1912_04822_b200 import GridMaker, errors
+
+        errors.use_exception_classes(voxmol.errors)  # callers catch voxmol's classes
 
         vz.GridMaker = GridMaker
         voxmol.GridMaker = GridMaker
