@@ -159,6 +159,51 @@ gm_status gm_backward(const gm_params *p, const gm_batch *b, const void *workspa
 /* Transformed coordinates computed by gm_prepare: (natoms,3) f64 device view. */
 const double *gm_workspace_positions(const void *workspace);
 
+/* ---- device-resident datasets: batch assembly on the device ----
+ *
+ * Replaces the per-call host packing of the reference's GridMaker._run_batch
+ * (voxelizer.py:372-435, fed by ExampleProvider.next_batch, sampling.py:364-380)
+ * for examples already resident in HBM: a batch is an index list, and
+ * gm_assemble builds the index-mode gm_batch arrays (sets, channel grouping,
+ * slot records, launch order) and the forward job table on the device.
+ *
+ * Dataset atom record (32 B, gm_dataset.records), per example in channel order
+ * (stable: atom order within a channel): f32 x, y, z, radius (unscaled);
+ * int32 local atom index (set order), absolute channel within the example,
+ * local backward launch rank, local set index | single-atom-set flag << 16. */
+typedef struct {
+    int32_t nexamples;               /* examples in the dataset */
+    int32_t nchannels;               /* channels of every example */
+    int32_t natoms, nsets;           /* totals */
+    const void *records;             /* device (natoms) 32-B atom records */
+    const int32_t *ex_atom_off;      /* device (nexamples+1) record offsets */
+    const int32_t *ex_set_off;       /* device (nexamples+1) set-table offsets */
+    const int32_t *ex_chan_off;      /* device (nexamples*(nchannels+1)), local to the example */
+    const int32_t *set_aoff;         /* device (nsets) first atom of the set, local */
+    const int32_t *set_natoms, *set_choff, *set_t; /* device (nsets) */
+    /* host mirrors (batch sizes are computed on the host without a sync) */
+    const int32_t *h_ex_atom_off;    /* (nexamples+1) */
+    const int32_t *h_ex_set_off;     /* (nexamples+1) */
+    const int32_t *h_ex_nzch;        /* (nexamples) channels with atoms */
+    const int32_t *h_ex_maxch;       /* (nexamples) largest channel */
+} gm_dataset;
+
+/* Assemble dataset examples ids[0..n) (host array) into the index-mode batch
+ * b: the caller fills b's device array pointers (coords32, atom_radius,
+ * atom_set, atom_type, set_start/end/example/choff/t, ex_item_start/end,
+ * item_perm, chan_off, bwd_slot, slot_rec, segs, origins) with room for
+ * atom_capacity atoms and set_capacity sets (segs: n*nchannels); gm_assemble
+ * writes the arrays on `stream` and sets b's counts (nexamples, nsets,
+ * natoms, nitems, nchannels, max_example_items, nsegs, max_seg_items) and
+ * its forward job table (jobs: device, jobs_capacity entries of 4 int32 --
+ * the same table gm_forward_jobs builds on the host).  Radii are scaled by
+ * p->radius_scale in f64 like voxelizer.py:430.  The batch equals the host
+ * packing of the same examples except for the backward launch order
+ * (per example here), which never changes results. */
+gm_status gm_assemble(const gm_params *p, const gm_dataset *ds, const int32_t *ids, int32_t n,
+                      gm_batch *b, int32_t atom_capacity, int32_t set_capacity,
+                      int32_t *jobs, int32_t jobs_capacity, void *stream);
+
 /* ---- reference-shaped kernels (argument meaning as _kernels.py) ---- */
 
 /* _kernels.forward_index_sets(out, coords, radii, tidx, set_start, set_end,
@@ -219,7 +264,7 @@ gm_status gm_draw_transforms(const double *u, int64_t n, int32_t rotation, doubl
 const char *gm_last_error(void);
 const char *gm_version(void);
 int32_t gm_device_count(void);
-/* sizeof(gm_params) (which = 0) or sizeof(gm_batch) (which = 1): ABI check for bindings. */
+/* sizeof(gm_params) (which = 0), gm_batch (1) or gm_dataset (2): ABI check for bindings. */
 int32_t gm_struct_size(int32_t which);
 /* Kernel launches issued by this process since the last reset (bench evidence). */
 int64_t gm_launch_count(int32_t reset);

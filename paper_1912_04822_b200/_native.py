@@ -63,6 +63,18 @@ class GmBatch(ctypes.Structure):
     ]
 
 
+class GmDataset(ctypes.Structure):
+    """Mirror of ``gm_dataset`` (device pointers and host mirrors as integers)."""
+
+    _fields_ = [
+        ("nexamples", _c_int32), ("nchannels", _c_int32), ("natoms", _c_int32),
+        ("nsets", _c_int32),
+        ("records", _vp), ("ex_atom_off", _vp), ("ex_set_off", _vp), ("ex_chan_off", _vp),
+        ("set_aoff", _vp), ("set_natoms", _vp), ("set_choff", _vp), ("set_t", _vp),
+        ("h_ex_atom_off", _vp), ("h_ex_set_off", _vp), ("h_ex_nzch", _vp), ("h_ex_maxch", _vp),
+    ]
+
+
 _LIB = None
 INLINE_MAX_EXAMPLES = 200  # GM_INLINE_MAX_EXAMPLES
 
@@ -71,6 +83,7 @@ EXPORTS = (
     "gm_forward_index_sets_host", "gm_forward_vector_sets_host", "gm_backward_index_host",
     "gm_backward_vector_host", "gm_last_error", "gm_version", "gm_device_count",
     "gm_launch_count", "gm_struct_size", "gm_draw_transforms", "gm_forward_jobs",
+    "gm_assemble",
 )
 
 
@@ -117,6 +130,9 @@ def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     L.gm_backward_vector_host.restype = ctypes.c_int
     L.gm_forward_jobs.argtypes = [P(GmParams), _c_int32, _c_int32, _vp, _vp, _c_int32]
     L.gm_forward_jobs.restype = _c_int32
+    L.gm_assemble.argtypes = [P(GmParams), P(GmDataset), _vp, _c_int32, P(GmBatch), _c_int32,
+                              _c_int32, _vp, _c_int32, _vp]
+    L.gm_assemble.restype = ctypes.c_int
     L.gm_draw_transforms.argtypes = [_vp, _c_int64, _c_int32, _c_double, _vp, _vp]
     L.gm_draw_transforms.restype = ctypes.c_int
     L.gm_last_error.restype = ctypes.c_char_p
@@ -125,7 +141,8 @@ def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     L.gm_struct_size.argtypes = [_c_int32]
     L.gm_struct_size.restype = _c_int32
     if L.gm_struct_size(0) != ctypes.sizeof(GmParams) or \
-            L.gm_struct_size(1) != ctypes.sizeof(GmBatch):
+            L.gm_struct_size(1) != ctypes.sizeof(GmBatch) or \
+            L.gm_struct_size(2) != ctypes.sizeof(GmDataset):
         raise DeviceError("ABI mismatch between _native.py and libgridmaker_b200.so")
     L.gm_launch_count.argtypes = [_c_int32]
     L.gm_launch_count.restype = _c_int64

@@ -518,7 +518,155 @@ gm_status launch(const FwdArgs &A, const FwdConfig &cfg, int nex, int njobs, cud
     return GM_OK;
 }
 
+// ---------------------------------------------------------------------------
+// The forward job table built on the device (batches assembled on the device
+// change composition every call; the host builder, forward_jobs_impl below,
+// costs milliseconds).  Same table, entry for entry: work jobs ordered by
+// (channel item count descending, example, tile, channel) and dealt GM_FWD_ALT_H
+// heavy : GM_FWD_ALT_L light, zero groups spread evenly -- each job's final
+// slot is computed in closed form from per-group ranks, so the table needs
+// no sort.
+// ---------------------------------------------------------------------------
+struct JobGeom {
+    int ntiles, ntj, TI, TJ;
+    int reorder;               // D <= GM_FWD_LPT_MAXD: GM_FWD_LPT (1 sorted, 2 dealt), else 0
+    long long W, Z, n;         // work jobs, zero jobs, total
+    long long H;               // heavy slots of the dealing
+};
+
+// One warp per (example, channel) group: ranks of the group among all groups.
+__global__ void __launch_bounds__(256) k_job_stats(const int32_t *co, int nex, int nch,
+                                                   int4 *stats) {
+    const int lane = threadIdx.x & 31;
+    const int g = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (g >= nex * nch) return;
+    const int e = g / nch, c = g - e * nch;
+    const int cnt = co[e * (nch + 1) + c + 1] - co[e * (nch + 1) + c];
+    int gt = 0, eqb = 0, eqe = 0, eqc = 0, nwb = 0, nwe = 0, nwc = 0;
+    for (int e2 = 0; e2 < nex; e2++) {
+        const int32_t *r = co + e2 * (nch + 1);
+        for (int c2 = lane; c2 < nch; c2 += 32) {
+            const int k = r[c2 + 1] - r[c2];
+            const bool before = e2 < e, same = e2 == e, cb = same && c2 < c;
+            if (cnt > 0) {
+                gt += k > cnt;
+                eqb += k == cnt && before;
+                eqe += k == cnt && same;
+                eqc += k == cnt && cb;
+                nwb += k > 0 && before;
+                nwe += k > 0 && same;
+                nwc += k > 0 && cb;
+            } else {  // zero groups: rank among zero groups
+                eqb += k == 0 && before;
+                eqe += k == 0 && same;
+                eqc += k == 0 && cb;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        gt += __shfl_xor_sync(0xffffffffu, gt, o);
+        eqb += __shfl_xor_sync(0xffffffffu, eqb, o);
+        eqe += __shfl_xor_sync(0xffffffffu, eqe, o);
+        eqc += __shfl_xor_sync(0xffffffffu, eqc, o);
+        nwb += __shfl_xor_sync(0xffffffffu, nwb, o);
+        nwe += __shfl_xor_sync(0xffffffffu, nwe, o);
+        nwc += __shfl_xor_sync(0xffffffffu, nwc, o);
+    }
+    if (lane == 0) {
+        stats[2 * g] = make_int4(gt, eqb, eqe, eqc);
+        stats[2 * g + 1] = make_int4(nwb, nwe, nwc, cnt);
+    }
+}
+
+// zeros before table slot k: floor(k Z / n) (the host rule places zero job
+// zi at the first slot k with (zi + 1) n <= (k + 1) Z)
+__device__ __forceinline__ long long zeros_before(long long k, const JobGeom &J) {
+    return J.Z ? (k * J.Z) / J.n : 0;
+}
+
+// One thread per (group, tile): the job's final slot.
+__global__ void __launch_bounds__(256) k_job_place(int nex, int nch, const int4 *stats,
+                                                   int4 *jobs, const JobGeom J) {
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (long long)nex * nch * J.ntiles) return;
+    const int g = (int)(idx / J.ntiles), t = (int)(idx - (long long)g * J.ntiles);
+    const int e = g / nch, c = g - e * nch;
+    const int4 s0 = stats[2 * g], s1 = stats[2 * g + 1];
+    long long k;
+    if (s1.w > 0) {
+        // rank in the sorted work list, then its slot in the heavy/light deal
+        long long srt, m;
+        if (J.reorder) {
+            srt = (long long)J.ntiles * (s0.x + s0.y) + (long long)t * s0.z + s0.w;
+            if (J.reorder == 1) {
+                m = srt;  // heaviest first, no dealing
+            } else if (srt < J.H) {
+                m = (long long)(GM_FWD_ALT_H + GM_FWD_ALT_L) * (srt / GM_FWD_ALT_H) + srt % GM_FWD_ALT_H;
+            } else {
+                const long long i = J.W - 1 - srt;  // i-th light job from the end
+                m = (long long)(GM_FWD_ALT_H + GM_FWD_ALT_L) * (i / GM_FWD_ALT_L) + GM_FWD_ALT_H +
+                    i % GM_FWD_ALT_L;
+            }
+        } else {
+            m = (long long)J.ntiles * s1.x + (long long)t * s1.y + s1.z;
+        }
+        // work job m sits at the last slot k with k - zeros_before(k) == m
+        long long lo = m, hi = J.n - 1;
+        while (lo < hi) {  // smallest k with (k + 1) - zeros_before(k + 1) > m
+            const long long mid = (lo + hi) >> 1;
+            if ((mid + 1) - zeros_before(mid + 1, J) > m) hi = mid;
+            else lo = mid + 1;
+        }
+        k = lo;
+    } else {
+        if (t % GM_FWD_ZGROUP) return;
+        const long long nzt = (J.ntiles + GM_FWD_ZGROUP - 1) / GM_FWD_ZGROUP;
+        const long long zi = nzt * s0.y + (long long)(t / GM_FWD_ZGROUP) * s0.z + s0.w;
+        k = ((zi + 1) * J.n + J.Z - 1) / J.Z - 1;  // ceil((zi + 1) n / Z) - 1
+    }
+    jobs[k] = make_int4(e, c, t, ((t / J.ntj) * J.TI) | (((t % J.ntj) * J.TJ) << 16));
+}
+
 }  // namespace
+
+// Job count of a grid size for the given numbers of (example, channel) groups
+// with and without items (gm_forward_jobs' table length).
+long long forward_job_count(int D, long long work_groups, long long zero_groups) {
+    const FwdConfig cfg = choose_config(D);
+    const long long ntiles = (long long)((D + cfg.TI - 1) / cfg.TI) * ((D + cfg.TJ - 1) / cfg.TJ);
+    return ntiles * work_groups + (ntiles + GM_FWD_ZGROUP - 1) / GM_FWD_ZGROUP * zero_groups;
+}
+
+gm_status forward_jobs_device(const gm_params *p, int nex, int nch, const int32_t *chan_off,
+                              int32_t *jobs, long long work_groups, long long zero_groups,
+                              int4 *stats, cudaStream_t s) {
+    const int D = p->npts;
+    const FwdConfig cfg = choose_config(D);
+    JobGeom J;
+    J.ntj = (D + cfg.TJ - 1) / cfg.TJ;
+    J.ntiles = ((D + cfg.TI - 1) / cfg.TI) * J.ntj;
+    J.TI = cfg.TI;
+    J.TJ = cfg.TJ;
+    J.reorder = D <= GM_FWD_LPT_MAXD ? GM_FWD_LPT : 0;
+    J.W = (long long)J.ntiles * work_groups;
+    J.Z = (J.ntiles + GM_FWD_ZGROUP - 1) / GM_FWD_ZGROUP * zero_groups;
+    J.n = J.W + J.Z;
+    // heavy slots of the deal: one per GM_FWD_ALT_H + GM_FWD_ALT_L, partial blocks included
+    {
+        const long long blk = GM_FWD_ALT_H + GM_FWD_ALT_L;
+        J.H = J.W / blk * GM_FWD_ALT_H + std::min<long long>(J.W % blk, GM_FWD_ALT_H);
+    }
+    const int G = nex * nch;
+    if (G == 0 || J.n == 0) return GM_OK;
+    k_job_stats<<<(G + 7) / 8, 256, 0, s>>>(chan_off, nex, nch, stats);
+    LAUNCH_CHECK();
+    const long long nt = (long long)G * J.ntiles;
+    k_job_place<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(nex, nch, stats,
+                                                            reinterpret_cast<int4 *>(jobs), J);
+    LAUNCH_CHECK();
+    return GM_OK;
+}
 
 gm_status forward_impl(const gm_params *p, const gm_batch *b, const Workspace &ws, float *out,
                        cudaStream_t s, bool *launched) {
