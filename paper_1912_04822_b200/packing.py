@@ -110,7 +110,9 @@ class PackedBatch:
                     atom_type[a0:a1] = cs.type_index
                 self.placed.append((e, choff, cs, int(a0), -1))
             L.add("atom_type", atom_type)
-            slot = _bwd_slots(coords, self.atom_example, self.default_centers)
+            slot = _bwd_slots(coords, self.atom_example, self.default_centers,
+                              slab=self.atom_example.astype(np.int64) * max(self.nchannels, 1) +
+                              set_choff[atom_set] + atom_type if self.natoms else None)
             self._bwd_slot_host = slot
             if slot is not None:
                 L.add("bwd_slot", slot)
@@ -427,15 +429,16 @@ _SLOT_DTYPE = np.dtype([("x", "<f4"), ("y", "<f4"), ("z", "<f4"), ("atom", "<i4"
                         ("pad", "<f8")])
 assert _SLOT_DTYPE.itemsize == 48
 
-# GM_BWD_ORDER: backward launch order of the atoms -- "lpt" (default: heaviest
-# first; measured best, C2 100 -> 94.5 us; vector mode orders within each
-# example, C4 374 -> 349 us), "lpt_local" (within examples), "alt" (heavy /
-# light alternating)
-# or "none" (atom order)
-_BWD_ORDER = os.environ.get("GM_BWD_ORDER", "lpt")
+# GM_BWD_ORDER: backward launch order of the atoms -- "slab" (default: grouped
+# by (example, channel) grid_grad slab, nearest the center first within a slab;
+# tools/bwd_order_ab.sh: C2 94.7 us, C5 DRAM reads halved), "lpt" (heaviest
+# first over the whole batch: C2 96.6 us), "lpt_local" (within examples; vector
+# mode always orders within each example, C4 374 -> 349 us), "alt" (heavy /
+# light alternating) or "none" (atom order)
+_BWD_ORDER = os.environ.get("GM_BWD_ORDER", "slab")
 
 
-def _bwd_slots(coords, atom_example, centers, per_example=False):
+def _bwd_slots(coords, atom_example, centers, per_example=False, slab=None):
     """Launch slot of each atom for the index-mode backward (gm_batch.bwd_slot).
 
     An atom's backward cost is its cutoff sphere's overlap with the grid, which
@@ -455,6 +458,11 @@ def _bwd_slots(coords, atom_example, centers, per_example=False):
     per_example = per_example or _BWD_ORDER == "lpt_local"
     if per_example:
         key = atom_example.astype(np.int64) * 32768 + key
+    elif _BWD_ORDER == "slab" and slab is not None:
+        # the atoms of one (example, channel) grid_grad slab together, nearest
+        # first: overlapping spheres re-read the slab from L2 (C5 DRAM reads
+        # 1152 -> 552 MB, 3.5x -> 1.7x the footprint; times unchanged)
+        key = slab.astype(np.int64) * 32768 + key
     order = np.argsort(key, kind="stable")
     if _BWD_ORDER == "alt":
         alt = np.empty(n, np.int64)
