@@ -61,12 +61,6 @@ __device__ __forceinline__ float approx_sqrt(float x) {
     return y;
 }
 
-__device__ __forceinline__ float approx_rsqrt(float x) {
-    float y;
-    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
 // 1/sqrt(d2) to ~1e-13 relative: the f64 MUFU estimate (MUFU.RSQ64H, ~2^-22)
 // + one f64 Newton step -- one XU op, no f32 <-> f64 conversions.
 __device__ __forceinline__ double rsqrt_d(double d2) {
@@ -102,18 +96,9 @@ __device__ __forceinline__ double exp_nonpos(double x) {
 }
 
 // Exact float -> double widening on the integer pipe (F2F.F64.F32 runs on the
-// XU, the backward's bottleneck).  Zeros and denormals map to signed zero
-// (grid gradients below 1e-38 contribute nothing at f32 output precision);
-// inf / NaN are not expected in gradients.
-// Masked variant: 0.0 unless `keep` -- branch-free (two extra LOPs).
-__device__ __forceinline__ double widen_if(float f, bool keep) {
-    const unsigned u = __float_as_uint(f);
-    const unsigned m = ((u & 0x7f800000u) != 0u && keep) ? 0xffffffffu : 0u;
-    const unsigned hi = ((u & 0x80000000u) | (((u >> 3) & 0x0fffffffu) + (896u << 20))) & m;
-    const unsigned lo = (u << 29) & m;
-    return __hiloint2double((int)hi, (int)lo);
-}
-
+// XU).  Zeros and denormals map to signed zero (grid gradients below 1e-38
+// contribute nothing at f32 output precision); inf / NaN are not expected in
+// gradients.  The index walk converts with F2F (measured faster there).
 __device__ __forceinline__ double widen(float f) {
     const unsigned u = __float_as_uint(f);
     const bool nz = (u & 0x7f800000u) != 0u;
@@ -202,9 +187,6 @@ constexpr int kBwdWarps = GM_BWD_WARPS;
 #ifndef GM_BWD_CHAINS
 #define GM_BWD_CHAINS 1
 #endif
-#ifndef GM_BWD_F2F
-#define GM_BWD_F2F 1  // widen grid gradients with F2F (XU) instead of integer ops
-#endif
 #ifndef GM_BWD_PREFETCH
 #define GM_BWD_PREFETCH 1  // L2 prefetch of each row span in phase 1 (C5 438 -> 424 us)
 #endif
@@ -216,9 +198,6 @@ constexpr int kBwdWarps = GM_BWD_WARPS;
 #endif
 #ifndef GM_BWD_SPLITSUM
 #define GM_BWD_SPLITSUM 1  // multi-value warp sums for the per-atom gradient epilogues
-#endif
-#ifndef GM_BWD_TAIL
-#define GM_BWD_TAIL 1  // index backward: single-window steps for the tail of each chunk
 #endif
 #ifndef GM_BWDV_D48
 #define GM_BWDV_D48 1  // vector backward specialised for 14 channels on 48^3 grids
@@ -535,7 +514,6 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
                         pdl_wait();
                         int cur = -1;  // rows started before the next window, minus one
                         const int last = total - 1;
-#if GM_BWD_TAIL
                         // U windows from base; the loop's tail runs one window
                         // at a time (no clamped dead windows).  Lane l still
                         // visits voxels l, l+32, ... in order: same sums.
@@ -567,11 +545,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
                                 // Ex Ey Ez (-4/r^2), tail 2 qa (d - dzr) / d; d2 = 0
                                 // takes the core branch and contributes 0 (dx=dy=dz=0)
                                 const double t = d2 <= d02 ? R.exy * zt.y : fma(-qa2dzr, rd, qa2);
-#if GM_BWD_F2F
                                 const double scl = (double)((vr <= last && d2 < dzr2) ? g[u] : 0.0f) * t;
-#else
-                                const double scl = widen_if(g[u], vr <= last && d2 < dzr2) * t;
-#endif
                                 gx = fma(scl, R.dx, gx);
                                 gy = fma(scl, R.dy, gy);
                                 gz = fma(scl, dz, gz);
@@ -581,45 +555,6 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
                         for (; base + 32 * kU <= total; base += 32 * kU)
                             step(std::integral_constant<int, kU>{}, base);
                         for (; base < total; base += 32) step(std::integral_constant<int, 1>{}, base);
-#else
-                        for (int base = 0; base < total; base += 32 * kU) {
-                            int myrow[kU];
-#pragma unroll
-                            for (int u = 0; u < kU; u++) {
-                                const unsigned M = W.starts[(base >> 5) + u];
-                                myrow[u] = cur + __popc(M & le);
-                                cur += __popc(M);
-                            }
-                            float g[kU];
-#pragma unroll
-                            for (int u = 0; u < kU; u++) {
-                                const int v = min(base + 32 * u + lane, last);
-                                g[u] = ld_gg<GM_BWD_GGHINT>(W.rows[myrow[u]].gp + v);
-                            }
-#pragma unroll
-                            for (int u = 0; u < kU; u++) {
-                                const int vr = base + 32 * u + lane;
-                                const int v = min(vr, last);
-                                const IRow &R = W.rows[myrow[u]];
-                                const double2 zt = W.zt[R.kz + v];
-                                const double dz = zt.x;
-                                const double d2 = fma(dz, dz, R.b2);
-                                const double rd = rsqrt_d(d2);
-                                // slope/d (_kernels.py:244-251): Gaussian core
-                                // Ex Ey Ez (-4/r^2), tail 2 qa (d - dzr) / d; d2 = 0
-                                // takes the core branch and contributes 0 (dx=dy=dz=0)
-                                const double t = d2 <= d02 ? R.exy * zt.y : fma(-qa2dzr, rd, qa2);
-#if GM_BWD_F2F
-                                const double scl = (double)((vr <= last && d2 < dzr2) ? g[u] : 0.0f) * t;
-#else
-                                const double scl = widen_if(g[u], vr <= last && d2 < dzr2) * t;
-#endif
-                                gx = fma(scl, R.dx, gx);
-                                gy = fma(scl, R.dy, gy);
-                                gz = fma(scl, dz, gz);
-                            }
-                        }
-#endif
                         __syncwarp();
                     }
                 }

@@ -155,8 +155,22 @@ inline size_t carve_workspace(void *base, int32_t natoms, int32_t nitems, int32_
 // clamped to [0, D-1] (the clamp keeps lo > hi for boxes that miss the grid).
 __device__ __forceinline__ void axis_bounds(double x, double cut, double origin, double res,
                                             int D, int &lo, int &hi) {
-    double l = ceil(__ddiv_rn(__dsub_rn(__dsub_rn(x, cut), origin), res));
-    double h = floor(__ddiv_rn(__dsub_rn(__dadd_rn(x, cut), origin), res));
+    const double nl = __dsub_rn(__dsub_rn(x, cut), origin);
+    const double nh = __dsub_rn(__dadd_rn(x, cut), origin);
+    double l, h;
+    // a power-of-two spacing (0.5, 0.25, 1 A ...): dividing by it is an exact
+    // scaling, so multiplying by its exact reciprocal gives the same bits
+    // without the DDIV sequence (warp-uniform branch)
+    const unsigned long long rb = (unsigned long long)__double_as_longlong(res);
+    const unsigned ex = (unsigned)(rb >> 52) & 0x7ffu;
+    if ((rb & 0x000fffffffffffffULL) == 0 && ex > 0 && ex < 2046 && !(rb >> 63)) {
+        const double inv = __longlong_as_double((long long)((2046ull - ex) << 52));
+        l = ceil(__dmul_rn(nl, inv));
+        h = floor(__dmul_rn(nh, inv));
+    } else {
+        l = ceil(__ddiv_rn(nl, res));
+        h = floor(__ddiv_rn(nh, res));
+    }
     l = fmin(fmax(l, 0.0), (double)D);
     h = fmax(fmin(h, (double)(D - 1)), -1.0);
     lo = (int)l;

@@ -16,8 +16,13 @@
 //   phase B (items in order): every lane reads the slot (broadcast) and
 //           scatters its (row, column) voxels: one FMA per row coordinate,
 //           d^2, ex2 (Gaussian core), sqrt (tail), a shared-memory accumulate.
-// Regions are disjoint and each warp adds its items in order, so every voxel
-// is summed in the reference's item order without atomics.  The finished tile
+// Regions are disjoint and each warp adds its items in order, without
+// atomics.  With the items in channel order (index typing on grids up to
+// 64^3) that is the reference's item order; where the prepare pass sorts each
+// channel's items by first plane (vector typing, grids above 64^3) a voxel's
+// sum runs bucket by bucket, item order within a bucket -- a fixed order (run
+// to run and batch-size independent), within the f32 tolerance of the
+// reference's.  The finished tile
 // (zeros included) leaves through TMA bulk stores (cp.async.bulk) when
 // D % 4 == 0: the planes of a tile are contiguous in global memory.  A
 // channel without items is written by one CTA (its tile 0) re-sending one

@@ -27,10 +27,10 @@
 struct PrepArgs;
 gm_status sort_planes(const PrepArgs &A, cudaStream_t s);
 
-// per-channel plane sort (k_sort_planes, k_prepare_seg)
+// per-channel plane sort (k_sort_planes): CTA sizes 64 / 128 / 256 threads,
+// each sorting up to kSortRounds items per thread in shared memory
 constexpr int kSortThreads = 256;  // the largest variant
 constexpr int kSortRounds = 4;
-constexpr int kSortMax = kSortThreads * kSortRounds;  // items per channel sorted in smem
 
 struct PrepArgs {
     gm_params p;

@@ -7,7 +7,7 @@ make_transform 121-136, transform_example 139-151).  The random draws and
 the rotation matrix are computed on the host with the reference's formulas
 so that a seeded stream yields bit-identical transforms; the per-atom
 application inside ``GridMaker.forward_batch`` runs on the GPU
-(``gm_prepare_*`` in csrc/gridmaker.cu) in the FMA order numpy's matmul uses
+(``k_prepare_static`` in csrc/prepare.cu) in the FMA order numpy's matmul uses
 on this host (see ``matmul_order``).
 """
 
@@ -145,7 +145,7 @@ def draw_transforms(centers, random_translation, random_rotation, rng) -> list:
     Draws every variate with one ``rng.random((N, k))`` call, which consumes
     the generator stream exactly as N sequential ``make_transform`` calls do
     (each takes 3 rotation then 3 translation doubles; ``uniform(-t, t)`` is
-    ``-t + 2t*u``).  ``tests/test_geom_host.py`` checks the equivalence.
+    ``-t + 2t*u``).  ``tests/test_cpu_host.py::test_draw_transforms_matches_sequential_make_transform`` checks the equivalence.
     """
     t = check_non_negative(random_translation, "random_translate")
     centers = np.asarray(centers, dtype=np.float64).reshape(-1, 3)
@@ -243,7 +243,7 @@ def transform_example(t: Transform, example):
 # numpy evaluates (x - c) @ R.T through BLAS; the FMA association of the
 # 3-term dot product depends on the BLAS kernel.  The
 # device reproduces it to keep binary occupancy bit-exact, so the order is
-# probed here once per process.  Codes (shared with csrc/gridmaker.cu):
+# probed here once per process.  Codes (shared with csrc/prepare.cu dot3):
 #   0..5  fma(a[p2],b[p2], fma(a[p1],b[p1], a[p0]*b[p0])) for permutation p
 #   6..8  unfused (a[p0]b[p0] + a[p1]b[p1]) + a[p2]b[p2]
 _PERMS = [(0, 1, 2), (1, 0, 2), (0, 2, 1), (2, 0, 1), (1, 2, 0), (2, 1, 0)]

@@ -5,7 +5,7 @@ Host-side mirror of the reference interface
 constructor, defaults, estimator protocol, geometry helpers, ``forward`` /
 ``forward_batch`` / ``backward`` semantics, validation order, exception
 classes and messages.  The arithmetic runs in the CUDA extension
-(csrc/gridmaker.cu) through the C ABI; there is no CPU path.
+(csrc/*.cu, libgridmaker_b200.so) through the C ABI; there is no CPU path.
 
 Additions:
 * ``backward_batch`` - batched backward over every set of every example in
