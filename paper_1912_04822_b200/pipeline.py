@@ -18,6 +18,7 @@ from __future__ import annotations
 import queue
 import threading
 
+import numpy as np
 import torch
 
 
@@ -111,3 +112,54 @@ class DeviceBatchPipeline:
 
     def __exit__(self, *exc):
         self.close()
+
+
+class DatasetBatches:
+    """Iterator of batches assembled on the device from a ``DeviceDataset``.
+
+    The device-resident counterpart of ``DeviceBatchPipeline``: examples
+    were uploaded once (dataset.py), so a batch is an index list and its
+    packing runs on the GPU (``gm_assemble``), stream-ordered, with nothing
+    left on the host to overlap.  ``shuffle`` draws a new permutation of the
+    dataset every epoch (``seed``); batches never straddle epochs -- the
+    last one of an epoch may be smaller unless ``drop_last``.  ``depth``
+    batch objects are recycled in a ring, so the ``depth - 1`` previous
+    batches stay valid while the next one is assembled.  Each yielded batch
+    carries ``ids`` (its dataset indices, in order).
+    """
+
+    def __init__(self, gm, dataset, batch_size: int, shuffle: bool = True, seed=None,
+                 depth: int = 2, drop_last: bool = False, max_batches=None):
+        self.gm = gm
+        self.dataset = dataset
+        self.batch_size = int(batch_size)
+        if not 1 <= self.batch_size <= dataset.nexamples:
+            raise ValueError(f"batch_size must be in 1..{dataset.nexamples}")
+        self.shuffle = bool(shuffle)
+        self.rng = np.random.default_rng(seed)
+        self.drop_last = bool(drop_last)
+        self.max_batches = max_batches
+        self._ring = [dataset.batch(self.batch_size) for _ in range(max(1, int(depth)))]
+        self._k = 0
+        self._order = None
+        self._pos = 0
+
+    def _next_ids(self):
+        n = self.dataset.nexamples
+        if self._order is None or self._pos >= n or \
+                (self.drop_last and self._pos + self.batch_size > n):
+            self._order = self.rng.permutation(n) if self.shuffle else np.arange(n)
+            self._pos = 0
+        ids = self._order[self._pos:self._pos + self.batch_size]
+        self._pos += ids.shape[0]
+        return ids
+
+    def __iter__(self):
+        return self
+
+    def __next__(self):
+        if self.max_batches is not None and self._k >= self.max_batches:
+            raise StopIteration
+        ab = self._ring[self._k % len(self._ring)]
+        self._k += 1
+        return ab.assemble(self.gm, self._next_ids())

@@ -1,7 +1,11 @@
 """Provider -> device batch pipeline: batches packed and
-uploaded ahead on a worker thread grid exactly like forward_batch."""
+uploaded ahead on a worker thread, and batches assembled on the device from
+a resident dataset, checked against the CPU oracle on the same examples."""
 import numpy as np
 import pytest
+
+import oracle
+from parity import assert_close
 
 torch = pytest.importorskip("torch")
 
@@ -32,11 +36,14 @@ def test_pipeline_batches_grid_like_forward_batch():
 
     gm = GridMaker()
     seen = 0
+    go = oracle.GridOracle()
     with DeviceBatchPipeline(gm, _Provider(21), batch_size=4, depth=2, max_batches=3) as pipe:
         for pb in pipe:
             grid, _ = gm.forward_packed(pb)
-            want = gm.forward_batch(pb.examples)
-            np.testing.assert_array_equal(grid.cpu().numpy(), want)
+            assert_close(grid.cpu().numpy(), go.forward_batch(pb.examples),
+                         what="pipeline batch vs oracle")
+            # and the same bits as the one-shot API
+            np.testing.assert_array_equal(grid.cpu().numpy(), gm.forward_batch(pb.examples))
             seen += 1
     assert seen == 3
 
@@ -58,3 +65,37 @@ def test_pipeline_from_iterable_and_errors():
         next(pipe)
         with pytest.raises(RuntimeError, match="provider failed"):
             next(pipe)
+
+
+def test_dataset_batches_epochs_and_parity():
+    """DatasetBatches: shuffled epochs over a device-resident dataset, each
+    batch assembled on the GPU; grids and gradients vs the oracle."""
+    from paper_1912_04822_b200 import GridMaker, geom, synthetic
+    from paper_1912_04822_b200.dataset import DeviceDataset
+    from paper_1912_04822_b200.pipeline import DatasetBatches
+
+    rng = np.random.default_rng(31)
+    exs = [synthetic.complex_example(rng, n_receptor=200) for _ in range(10)]
+    gm = GridMaker()
+    ds = DeviceDataset(exs)
+    it = DatasetBatches(gm, ds, batch_size=4, seed=5, depth=2)
+    seen = []
+    go = oracle.GridOracle()
+    for k in range(6):  # two epochs of 4 + 4 + 2
+        ab = next(it)
+        sub = [exs[i] for i in ab.ids]
+        seen.append(list(ab.ids))
+        xf = geom.draw_transform_array(ab.default_centers, 1.5, True, np.random.default_rng(k))
+        grid, _ = gm.forward_packed(ab, transforms=xf)
+        ref = go.forward_batch(sub, random_rotation=True, random_translation=1.5,
+                               rng=np.random.default_rng(k))
+        assert_close(grid.cpu().numpy(), ref, what=f"batch {k}")
+        gg = torch.from_numpy(ref).cuda()
+        cg, _ = gm.backward_packed(ab, gg, reuse_prepared=True)
+        cgs, _ = go.backward_batch(sub, ref, random_rotation=True, random_translation=1.5,
+                                   rng=np.random.default_rng(k))
+        assert_close(cg.cpu().numpy(), np.concatenate(cgs), what=f"batch {k} gradients")
+    assert [len(s) for s in seen] == [4, 4, 2, 4, 4, 2]
+    assert sorted(sum(seen[:3], [])) == list(range(10))
+    assert sorted(sum(seen[3:], [])) == list(range(10))
+    assert seen[:3] != seen[3:]  # a new permutation each epoch
