@@ -7,7 +7,7 @@
 // ExampleProvider.next_batch (sampling.py:364-380).  Here the examples live in
 // HBM already grouped by channel (the grouping of a batch is the
 // concatenation of its examples' groupings), so a batch is an index list:
-// one CTA per batch example copies its 32-B atom records into the packed
+// CTAs per (batch example, 256-atom chunk) copy its 32-B atom records into the packed
 // arrays the prepare pass reads (slot records in channel order, atoms in set
 // order), writes its set rows, channel offsets and nonzero-channel list.  The
 // forward job table follows on the device (forward.cu: k_job_stats /
@@ -42,8 +42,13 @@ struct AsmArgs {
     int4 ex[GM_INLINE_MAX_EXAMPLES];  // per batch example: id, atom base, set base, seg base
 };
 
+// grid (batch example, atom chunk of kAsmChunk): chunk 0 also writes the
+// example's set rows, channel offsets and nonzero-channel list
+constexpr int kAsmChunk = 256;
+
 __global__ void __launch_bounds__(256) k_assemble(const __grid_constant__ AsmArgs A) {
     const int bi = blockIdx.x, tid = threadIdx.x;
+    const int q0 = blockIdx.y * kAsmChunk;
     const int4 X = A.ex[bi];
     const int id = X.x, abase = X.y, sbase = X.z, gbase = X.w;
     const gm_dataset &ds = A.ds;
@@ -51,40 +56,43 @@ __global__ void __launch_bounds__(256) k_assemble(const __grid_constant__ AsmArg
     const int C = ds.nchannels;
     const int a0 = ds.ex_atom_off[id], na = ds.ex_atom_off[id + 1] - a0;
     const int s0 = ds.ex_set_off[id], ns = ds.ex_set_off[id + 1] - s0;
-    // set rows (voxelizer.py:388-395 layout)
-    for (int t = tid; t < ns; t += blockDim.x) {
-        const int st = abase + ds.set_aoff[s0 + t];
-        int32_t *w = const_cast<int32_t *>(b.set_start);
-        w[sbase + t] = st;
-        const_cast<int32_t *>(b.set_end)[sbase + t] = st + ds.set_natoms[s0 + t];
-        const_cast<int32_t *>(b.set_example)[sbase + t] = bi;
-        const_cast<int32_t *>(b.set_choff)[sbase + t] = ds.set_choff[s0 + t];
-        const_cast<int32_t *>(b.set_t)[sbase + t] = ds.set_t[s0 + t];
-    }
-    if (tid == 0) {
-        const_cast<int32_t *>(b.ex_item_start)[bi] = abase;
-        const_cast<int32_t *>(b.ex_item_end)[bi] = abase + na;
-    }
-    // channel offsets and the groups with items (gm_batch.segs, ascending)
-    const int32_t *lco = ds.ex_chan_off + (size_t)id * (C + 1);
-    for (int c = tid; c <= C; c += blockDim.x)
-        const_cast<int32_t *>(b.chan_off)[(size_t)bi * (C + 1) + c] = abase + lco[c];
-    if (tid < 32) {
-        int carry = 0;
-        for (int c0 = 0; c0 < C; c0 += 32) {
-            const int c = c0 + tid;
-            const bool nz = c < C && lco[c + 1] > lco[c];
-            const unsigned m = __ballot_sync(0xffffffffu, nz);
-            if (nz)
-                const_cast<int32_t *>(b.segs)[gbase + carry + __popc(m & ((1u << tid) - 1u))] =
-                    bi * C + c;
-            carry += __popc(m);
+    if (q0 >= na && blockIdx.y > 0) return;
+    if (blockIdx.y == 0) {
+        // set rows (voxelizer.py:388-395 layout)
+        for (int t = tid; t < ns; t += blockDim.x) {
+            const int st = abase + ds.set_aoff[s0 + t];
+            int32_t *w = const_cast<int32_t *>(b.set_start);
+            w[sbase + t] = st;
+            const_cast<int32_t *>(b.set_end)[sbase + t] = st + ds.set_natoms[s0 + t];
+            const_cast<int32_t *>(b.set_example)[sbase + t] = bi;
+            const_cast<int32_t *>(b.set_choff)[sbase + t] = ds.set_choff[s0 + t];
+            const_cast<int32_t *>(b.set_t)[sbase + t] = ds.set_t[s0 + t];
         }
-    }
+        if (tid == 0) {
+            const_cast<int32_t *>(b.ex_item_start)[bi] = abase;
+            const_cast<int32_t *>(b.ex_item_end)[bi] = abase + na;
+        }
+        // channel offsets and the groups with items (gm_batch.segs, ascending)
+        const int32_t *lco = ds.ex_chan_off + (size_t)id * (C + 1);
+        for (int c = tid; c <= C; c += blockDim.x)
+            const_cast<int32_t *>(b.chan_off)[(size_t)bi * (C + 1) + c] = abase + lco[c];
+        if (tid < 32) {
+            int carry = 0;
+            for (int c0 = 0; c0 < C; c0 += 32) {
+                const int c = c0 + tid;
+                const bool nz = c < C && lco[c + 1] > lco[c];
+                const unsigned m = __ballot_sync(0xffffffffu, nz);
+                if (nz)
+                    const_cast<int32_t *>(b.segs)[gbase + carry + __popc(m & ((1u << tid) - 1u))] =
+                        bi * C + c;
+                carry += __popc(m);
+            }
+        }
+    }  // chunk 0
     // atoms: slot records in channel order, per-atom arrays in set order
     const DsAtom *rec = reinterpret_cast<const DsAtom *>(ds.records) + a0;
     SlotOut *slot = reinterpret_cast<SlotOut *>(const_cast<void *>(b.slot_rec)) + abase;
-    for (int q = tid; q < na; q += blockDim.x) {
+    for (int q = q0 + tid; q < min(na, q0 + kAsmChunk); q += blockDim.x) {
         const DsAtom R = rec[q];
         const int a = abase + R.atom;
         const int sl = R.set_single & 0xffff;
@@ -165,7 +173,7 @@ gm_status assemble_impl(const gm_params *p, const gm_dataset *ds, const int32_t 
     b->nfwd_jobs = (int32_t)njobs;
     b->fwd_jobs_npts = p->npts;
     A.b = *b;
-    k_assemble<<<n, 256, 0, s>>>(A);
+    k_assemble<<<dim3(n, (unsigned)std::max(1, (maxex + kAsmChunk - 1) / kAsmChunk)), 256, 0, s>>>(A);
     LAUNCH_CHECK();
     return forward_jobs_device(p, n, C, b->chan_off, jobs, nsegs, G - nsegs,
                                reinterpret_cast<int4 *>(jobs + 4 * njobs), s);

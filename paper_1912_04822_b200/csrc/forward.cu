@@ -540,32 +540,47 @@ struct JobGeom {
 };
 
 // One warp per (example, channel) group: ranks of the group among all groups.
+// The group item counts are staged in shared memory first (the rank loop
+// then runs on shared-memory reads instead of serial L2 round trips).
+constexpr int kJobStatsMaxG = 12288;  // groups staged in shared memory (48 KB)
 __global__ void __launch_bounds__(256) k_job_stats(const int32_t *co, int nex, int nch,
                                                    int4 *stats) {
+    __shared__ int cnt[kJobStatsMaxG];
+    const int G = nex * nch;
+    const bool staged = G <= kJobStatsMaxG;
+    if (staged)
+        for (int q = threadIdx.x; q < G; q += blockDim.x) {
+            const int e = q / nch, c = q - e * nch;
+            cnt[q] = co[e * (nch + 1) + c + 1] - co[e * (nch + 1) + c];
+        }
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const int g = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (g >= nex * nch) return;
+    if (g >= G) return;
     const int e = g / nch, c = g - e * nch;
-    const int cnt = co[e * (nch + 1) + c + 1] - co[e * (nch + 1) + c];
+    auto count_of = [&](int q) {
+        if (staged) return cnt[q];
+        const int e2 = q / nch, c2 = q - e2 * nch;
+        return co[e2 * (nch + 1) + c2 + 1] - co[e2 * (nch + 1) + c2];
+    };
+    const int k0 = count_of(g);
     int gt = 0, eqb = 0, eqe = 0, eqc = 0, nwb = 0, nwe = 0, nwc = 0;
-    for (int e2 = 0; e2 < nex; e2++) {
-        const int32_t *r = co + e2 * (nch + 1);
-        for (int c2 = lane; c2 < nch; c2 += 32) {
-            const int k = r[c2 + 1] - r[c2];
-            const bool before = e2 < e, same = e2 == e, cb = same && c2 < c;
-            if (cnt > 0) {
-                gt += k > cnt;
-                eqb += k == cnt && before;
-                eqe += k == cnt && same;
-                eqc += k == cnt && cb;
-                nwb += k > 0 && before;
-                nwe += k > 0 && same;
-                nwc += k > 0 && cb;
-            } else {  // zero groups: rank among zero groups
-                eqb += k == 0 && before;
-                eqe += k == 0 && same;
-                eqc += k == 0 && cb;
-            }
+    const int gfirst = e * nch;  // first group of this example
+    for (int q = lane; q < G; q += 32) {
+        const int k = count_of(q);
+        const bool before = q < gfirst, same = q >= gfirst && q < gfirst + nch, cb = same && q < g;
+        if (k0 > 0) {
+            gt += k > k0;
+            eqb += k == k0 && before;
+            eqe += k == k0 && same;
+            eqc += k == k0 && cb;
+            nwb += k > 0 && before;
+            nwe += k > 0 && same;
+            nwc += k > 0 && cb;
+        } else {  // zero groups: rank among zero groups
+            eqb += k == 0 && before;
+            eqe += k == 0 && same;
+            eqc += k == 0 && cb;
         }
     }
 #pragma unroll
@@ -580,7 +595,7 @@ __global__ void __launch_bounds__(256) k_job_stats(const int32_t *co, int nex, i
     }
     if (lane == 0) {
         stats[2 * g] = make_int4(gt, eqb, eqe, eqc);
-        stats[2 * g + 1] = make_int4(nwb, nwe, nwc, cnt);
+        stats[2 * g + 1] = make_int4(nwb, nwe, nwc, k0);
     }
 }
 
