@@ -355,6 +355,10 @@ def fresh_leg(args, cfg, gm, rank, ws, dev, stream, ev, barrier, out, tg, pool=1
     build_s = time.perf_counter() - t0
     ab = ds.batch(N)
     cap = ab.atom_capacity
+    # vector typing: type gradients stay on the device (the CNN's side), sized
+    # for the largest assembled batch
+    tg = torch.empty(max(ab._cap.weights, 1), dtype=torch.float32, device=dev) \
+        if ds.vector_mode else None
     cgs = [torch.empty((cap, 3), dtype=torch.float32, device=dev) for _ in range(2)]
     host_cg = [torch.empty((cap, 3), dtype=torch.float32, pin_memory=True) for _ in range(2)]
     copy_s = torch.cuda.Stream(device=dev)
@@ -381,7 +385,8 @@ def fresh_leg(args, cfg, gm, rank, ws, dev, stream, ev, barrier, out, tg, pool=1
         gm.forward_packed(ab, o, transforms=xf)
         cg = cgs[x][:ab.natoms]
         stream.wait_event(done[x])  # the D2H of two steps ago has read cgs[x]
-        gm.backward_packed(ab, o, reuse_prepared=True, coord_grad=cg, type_grad=tg)
+        gm.backward_packed(ab, o, reuse_prepared=True, coord_grad=cg,
+                           type_grad=tg[:max(ab.nweights, 1)] if tg is not None else None)
         ev_b = torch.cuda.Event()
         ev_b.record(stream)
         with torch.cuda.stream(copy_s):
@@ -589,7 +594,7 @@ def main():
     # ---- e2e_fresh: new, shuffled examples every step from a device-resident
     # dataset (DeviceDataset), each batch assembled on the device ----
     e2e_fresh = None
-    if not args.no_e2e and not cfg.get("ligand_only") and not cfg["vector"]:
+    if not args.no_e2e and not cfg.get("ligand_only"):
         e2e_fresh = fresh_leg(args, cfg, gm, rank, ws, dev, stream, ev, barrier, out, tg)
 
     # the reference-shaped API a numpy user switches to: forward_batch -> host

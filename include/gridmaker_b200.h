@@ -185,24 +185,47 @@ typedef struct {
     const int32_t *h_ex_atom_off;    /* (nexamples+1) */
     const int32_t *h_ex_set_off;     /* (nexamples+1) */
     const int32_t *h_ex_nzch;        /* (nexamples) channels with atoms */
-    const int32_t *h_ex_maxch;       /* (nexamples) largest channel */
+    const int32_t *h_ex_maxch;       /* (nexamples) largest channel (items in vector mode) */
+    /* vector typing (vector_mode = 1): records are in SET order (their channel
+     * field is unused); items are the nonzero weights, per example in item
+     * order (atom-major, channel-minor per set, _kernels.py:159-166), 16 B each:
+     * int32 local atom, channel within the set, f32 weight, the item's slot in
+     * the example's channel grouping; ex_chan_off counts ITEMS; weight rows and
+     * type radii per set as the CoordinateSets hold them (f32, unscaled). */
+    int32_t vector_mode;
+    int32_t nitems, nweights, ntype_radii; /* totals */
+    const void *items;               /* device (nitems) */
+    const float *weights;            /* device (nweights) */
+    const float *type_radii;         /* device (ntype_radii) */
+    const int32_t *ex_item_off, *ex_w_off, *ex_tr_off; /* device (nexamples+1) */
+    const int32_t *set_woff, *set_troff; /* device (nsets), local to the example */
+    const int32_t *h_ex_item_off, *h_ex_w_off, *h_ex_tr_off; /* host mirrors (nexamples+1) */
 } gm_dataset;
 
-/* Assemble dataset examples ids[0..n) (host array) into the index-mode batch
- * b: the caller fills b's device array pointers (coords32, atom_radius,
- * atom_set, atom_type, set_start/end/example/choff/t, ex_item_start/end,
- * item_perm, chan_off, bwd_slot, slot_rec, segs, origins) with room for
- * atom_capacity atoms and set_capacity sets (segs: n*nchannels); gm_assemble
- * writes the arrays on `stream` and sets b's counts (nexamples, nsets,
- * natoms, nitems, nchannels, max_example_items, nsegs, max_seg_items) and
- * its forward job table (jobs: device, jobs_capacity entries of 4 int32 --
- * the same table gm_forward_jobs builds on the host).  Radii are scaled by
- * p->radius_scale in f64 like voxelizer.py:430.  The batch equals the host
- * packing of the same examples except for the backward launch order
- * (per example here), which never changes results. */
+/* Capacities of the caller's batch arrays for gm_assemble. */
+typedef struct {
+    int32_t atoms, sets, items, weights, type_radii; /* items: vector mode (index: = atoms) */
+    int32_t jobs;                    /* forward job table entries (4 int32 each) + 2 per group */
+} gm_capacity;
+
+/* Assemble dataset examples ids[0..n) (host array) into the batch b: the
+ * caller fills b's device array pointers with room for cap's counts --
+ * index mode: coords32, atom_radius, atom_set, atom_type, set_start/end/
+ * example/choff/t, ex_item_start/end, item_perm, chan_off, bwd_slot,
+ * slot_rec, segs (n*nchannels), origins; vector mode: coords32, atom_radius,
+ * atom_set, set_*, set_wstart, set_trstart, weights, type_radius, item_atom,
+ * item_channel, item_weight, item_radius, ex_item_start/end, item_perm,
+ * chan_off, bwd_slot, segs, origins.  gm_assemble writes the arrays on
+ * `stream`, sets b's counts (nexamples, nsets, natoms, nitems, nweights,
+ * nchannels, vector_mode, max_example_items, nsegs, max_seg_items) and its
+ * forward job table (jobs: device, cap->jobs entries of 4 int32 -- the same
+ * table gm_forward_jobs builds on the host).  Radii (and type radii) are
+ * scaled by p->radius_scale in f64 like voxelizer.py:416,430; item radii
+ * follow p->radius_type_indexed.  The batch equals the host packing of the
+ * same examples (index mode: up to the backward launch order, per example
+ * here, which never changes results). */
 gm_status gm_assemble(const gm_params *p, const gm_dataset *ds, const int32_t *ids, int32_t n,
-                      gm_batch *b, int32_t atom_capacity, int32_t set_capacity,
-                      int32_t *jobs, int32_t jobs_capacity, void *stream);
+                      gm_batch *b, const gm_capacity *cap, int32_t *jobs, void *stream);
 
 /* ---- reference-shaped kernels (argument meaning as _kernels.py) ---- */
 
@@ -264,7 +287,7 @@ gm_status gm_draw_transforms(const double *u, int64_t n, int32_t rotation, doubl
 const char *gm_last_error(void);
 const char *gm_version(void);
 int32_t gm_device_count(void);
-/* sizeof(gm_params) (which = 0), gm_batch (1) or gm_dataset (2): ABI check for bindings. */
+/* sizeof(gm_params) (which = 0), gm_batch (1), gm_dataset (2) or gm_capacity (3): ABI check. */
 int32_t gm_struct_size(int32_t which);
 /* Kernel launches issued by this process since the last reset (bench evidence). */
 int64_t gm_launch_count(int32_t reset);

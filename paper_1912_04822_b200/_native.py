@@ -72,7 +72,20 @@ class GmDataset(ctypes.Structure):
         ("records", _vp), ("ex_atom_off", _vp), ("ex_set_off", _vp), ("ex_chan_off", _vp),
         ("set_aoff", _vp), ("set_natoms", _vp), ("set_choff", _vp), ("set_t", _vp),
         ("h_ex_atom_off", _vp), ("h_ex_set_off", _vp), ("h_ex_nzch", _vp), ("h_ex_maxch", _vp),
+        ("vector_mode", _c_int32), ("nitems", _c_int32), ("nweights", _c_int32),
+        ("ntype_radii", _c_int32),
+        ("items", _vp), ("weights", _vp), ("type_radii", _vp),
+        ("ex_item_off", _vp), ("ex_w_off", _vp), ("ex_tr_off", _vp),
+        ("set_woff", _vp), ("set_troff", _vp),
+        ("h_ex_item_off", _vp), ("h_ex_w_off", _vp), ("h_ex_tr_off", _vp),
     ]
+
+
+class GmCapacity(ctypes.Structure):
+    """Mirror of ``gm_capacity``."""
+
+    _fields_ = [("atoms", _c_int32), ("sets", _c_int32), ("items", _c_int32),
+                ("weights", _c_int32), ("type_radii", _c_int32), ("jobs", _c_int32)]
 
 
 _LIB = None
@@ -130,8 +143,8 @@ def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     L.gm_backward_vector_host.restype = ctypes.c_int
     L.gm_forward_jobs.argtypes = [P(GmParams), _c_int32, _c_int32, _vp, _vp, _c_int32]
     L.gm_forward_jobs.restype = _c_int32
-    L.gm_assemble.argtypes = [P(GmParams), P(GmDataset), _vp, _c_int32, P(GmBatch), _c_int32,
-                              _c_int32, _vp, _c_int32, _vp]
+    L.gm_assemble.argtypes = [P(GmParams), P(GmDataset), _vp, _c_int32, P(GmBatch),
+                              P(GmCapacity), _vp, _vp]
     L.gm_assemble.restype = ctypes.c_int
     L.gm_draw_transforms.argtypes = [_vp, _c_int64, _c_int32, _c_double, _vp, _vp]
     L.gm_draw_transforms.restype = ctypes.c_int
@@ -142,7 +155,8 @@ def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     L.gm_struct_size.restype = _c_int32
     if L.gm_struct_size(0) != ctypes.sizeof(GmParams) or \
             L.gm_struct_size(1) != ctypes.sizeof(GmBatch) or \
-            L.gm_struct_size(2) != ctypes.sizeof(GmDataset):
+            L.gm_struct_size(2) != ctypes.sizeof(GmDataset) or \
+            L.gm_struct_size(3) != ctypes.sizeof(GmCapacity):
         raise DeviceError("ABI mismatch between _native.py and libgridmaker_b200.so")
     L.gm_launch_count.argtypes = [_c_int32]
     L.gm_launch_count.restype = _c_int64

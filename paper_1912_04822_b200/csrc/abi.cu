@@ -197,29 +197,34 @@ extern "C" gm_status gm_forward(const gm_params *p, const gm_batch *b, const voi
 }
 
 gm_status assemble_impl(const gm_params *p, const gm_dataset *ds, const int32_t *ids, int32_t n,
-                        gm_batch *b, int32_t atom_capacity, int32_t set_capacity, int32_t *jobs,
-                        int32_t jobs_capacity, cudaStream_t s);
+                        gm_batch *b, const gm_capacity *cap, int32_t *jobs, cudaStream_t s);
 
 extern "C" gm_status gm_assemble(const gm_params *p, const gm_dataset *ds, const int32_t *ids,
-                                 int32_t n, gm_batch *b, int32_t atom_capacity,
-                                 int32_t set_capacity, int32_t *jobs, int32_t jobs_capacity,
+                                 int32_t n, gm_batch *b, const gm_capacity *cap, int32_t *jobs,
                                  void *stream) {
     gm_status st = check_params(p);
     if (st) return st;
-    if (!ds || !b || !ids || !jobs) return gm_fail(GM_ERR_INVALID, "NULL argument");
+    if (!ds || !b || !ids || !jobs || !cap) return gm_fail(GM_ERR_INVALID, "NULL argument");
     if (!ds->records || !ds->ex_atom_off || !ds->ex_set_off || !ds->ex_chan_off || !ds->set_aoff ||
         !ds->set_natoms || !ds->set_choff || !ds->set_t || !ds->h_ex_atom_off ||
         !ds->h_ex_set_off || !ds->h_ex_nzch || !ds->h_ex_maxch)
         return gm_fail(GM_ERR_INVALID, "dataset is missing arrays");
     if (ds->nchannels < 1 || ds->nchannels > 8192)
         return gm_fail(GM_ERR_INVALID, "dataset channel count %d", ds->nchannels);
-    if (!b->coords32 || !b->atom_radius || !b->atom_set || !b->atom_type || !b->set_start ||
-        !b->set_end || !b->set_example || !b->set_choff || !b->set_t || !b->ex_item_start ||
-        !b->ex_item_end || !b->item_perm || !b->chan_off || !b->bwd_slot || !b->slot_rec ||
-        !b->segs)
+    if (!b->coords32 || !b->atom_radius || !b->atom_set || !b->set_start || !b->set_end ||
+        !b->set_example || !b->set_choff || !b->set_t || !b->ex_item_start || !b->ex_item_end ||
+        !b->item_perm || !b->chan_off || !b->bwd_slot || !b->segs)
         return gm_fail(GM_ERR_INVALID, "batch is missing device arrays");
-    return assemble_impl(p, ds, ids, n, b, atom_capacity, set_capacity, jobs, jobs_capacity,
-                         (cudaStream_t)stream);
+    if (!ds->vector_mode && (!b->atom_type || !b->slot_rec))
+        return gm_fail(GM_ERR_INVALID, "index-mode batch needs atom_type and slot_rec");
+    if (ds->vector_mode &&
+        (!ds->items || !ds->weights || !ds->type_radii || !ds->ex_item_off || !ds->ex_w_off ||
+         !ds->ex_tr_off || !ds->set_woff || !ds->set_troff || !ds->h_ex_item_off ||
+         !ds->h_ex_w_off || !ds->h_ex_tr_off || !b->set_wstart || !b->set_trstart ||
+         !b->weights || !b->type_radius || !b->item_atom || !b->item_channel ||
+         !b->item_weight || !b->item_radius))
+        return gm_fail(GM_ERR_INVALID, "vector-mode dataset / batch is missing arrays");
+    return assemble_impl(p, ds, ids, n, b, cap, jobs, (cudaStream_t)stream);
 }
 
 extern "C" gm_status gm_backward(const gm_params *p, const gm_batch *b, const void *workspace,
@@ -659,6 +664,7 @@ extern "C" int32_t gm_struct_size(int32_t which) {
     return which == 0   ? (int32_t)sizeof(gm_params)
            : which == 1 ? (int32_t)sizeof(gm_batch)
            : which == 2 ? (int32_t)sizeof(gm_dataset)
+           : which == 3 ? (int32_t)sizeof(gm_capacity)
                         : -1;
 }
 extern "C" int64_t gm_launch_count(int32_t reset) {

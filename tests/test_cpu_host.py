@@ -33,6 +33,8 @@ def test_abi_struct_sizes_match_bindings():
     L = _native.load_library()
     assert L.gm_struct_size(0) == ctypes.sizeof(_native.GmParams)
     assert L.gm_struct_size(1) == ctypes.sizeof(_native.GmBatch)
+    assert L.gm_struct_size(2) == ctypes.sizeof(_native.GmDataset)
+    assert L.gm_struct_size(3) == ctypes.sizeof(_native.GmCapacity)
     assert L.gm_version().startswith(b"gridmaker_b200")
 
 

@@ -122,3 +122,85 @@ def test_assembled_forward_backward_bitwise_and_vs_oracle(data, cfg):
         cgs, _ = go.backward_batch(sub, gg.cpu().numpy(), random_rotation=True,
                                    random_translation=2.0, rng=np.random.default_rng(2))
         assert_close(cg.cpu().numpy(), np.concatenate(cgs), what="assembled backward vs oracle")
+
+
+@pytest.fixture(scope="module")
+def vdata():
+    from conftest import random_coordinate_set
+    from paper_1912_04822_b200 import Example, make_vector_types, synthetic
+    from paper_1912_04822_b200.dataset import DeviceDataset
+
+    exs = synthetic.batch(16, seed=4, vector=True)
+    rng = np.random.default_rng(6)
+    for k in range(4):  # odd shapes: single-atom and empty sets
+        a = make_vector_types(random_coordinate_set(rng, [1, 0, 9, 25][k], 14, 8.0))
+        b = make_vector_types(random_coordinate_set(rng, [7, 3, 0, 1][k], 14, 4.0))
+        exs.append(Example(coord_sets=[a, b]))
+    return exs, DeviceDataset(exs)
+
+
+@pytest.mark.parametrize("rti", [False, True])
+def test_vector_assembled_batch_equals_host_packing(vdata, rti):
+    from paper_1912_04822_b200 import GridMaker
+
+    exs, ds = vdata
+    gm = GridMaker(radius_type_indexed=rti)
+    # the odd examples (index >= 16) carry no type radii: type-indexed radii
+    # take the synthetic ones only, as the host packing requires
+    ids = np.random.default_rng(3).permutation(16 if rti else len(exs))[:13]
+    ab = ds.batch(16).assemble(gm, ids)
+    pb = gm.pack([exs[i] for i in ids])
+    torch.cuda.synchronize()
+    assert (ab.nexamples, ab.natoms, ab.nitems, ab.nsets, ab.nsegs, ab.max_seg_items,
+            ab.max_example_items, ab.nweights) == (pb.nexamples, pb.natoms, pb.nitems, pb.nsets,
+                                                   pb.nsegs, pb.max_seg_items,
+                                                   pb.max_example_items, pb.nweights)
+    A, S, N, C, I = pb.natoms, pb.nsets, pb.nexamples, pb.nchannels, pb.nitems
+    for name, n in (("coords32", 3 * A), ("atom_radius", A), ("atom_set", A),
+                    ("set_start", S), ("set_end", S), ("set_example", S), ("set_choff", S),
+                    ("set_t", S), ("set_wstart", S), ("set_trstart", S),
+                    ("weights", pb.nweights), ("type_radius", pb.offsets["type_radius"][2][0]),
+                    ("item_atom", I), ("item_channel", I), ("item_weight", I),
+                    ("item_radius", I), ("ex_item_start", N), ("ex_item_end", N),
+                    ("item_perm", I), ("chan_off", N * (C + 1)), ("segs", pb.nsegs),
+                    ("bwd_slot", A)):
+        np.testing.assert_array_equal(_dev_array(ab, name, n), _host_array(pb, name, n),
+                                      err_msg=name)
+
+
+@pytest.mark.parametrize("rti", [False, True])
+def test_vector_assembled_forward_backward(vdata, rti):
+    from paper_1912_04822_b200 import GridMaker, geom
+
+    exs, ds = vdata
+    gm = GridMaker(radius_type_indexed=rti)
+    ab = ds.batch(8)
+    ids = np.random.default_rng(8).permutation(16 if rti else len(exs))[:8]
+    ab.assemble(gm, ids)
+    sub = [exs[i] for i in ids]
+    xf = geom.draw_transform_array(ab.default_centers, 2.0, True, np.random.default_rng(4))
+    out, _ = gm.forward_packed(ab, transforms=xf)
+    gg = torch.randn_like(out)
+    cg, tg = gm.backward_packed(ab, gg, reuse_prepared=True)
+    pb = gm.pack(sub)
+    out2, _ = gm.forward_packed(pb, transforms=xf)
+    cg2, tg2 = gm.backward_packed(pb, gg, reuse_prepared=True)
+    assert torch.equal(out, out2)
+    assert torch.equal(cg, cg2) and torch.equal(tg, tg2)
+    go = oracle.GridOracle(radius_type_indexed=rti)
+    ref = go.forward_batch(sub, random_rotation=True, random_translation=2.0,
+                           rng=np.random.default_rng(4))
+    assert_close(out.cpu().numpy(), ref, what="vector assembled forward vs oracle")
+    cgs, tgs = go.backward_batch(sub, gg.cpu().numpy(), random_rotation=True,
+                                 random_translation=2.0, rng=np.random.default_rng(4))
+    assert_close(cg.cpu().numpy(), np.concatenate(cgs), what="coord grads")
+    assert_close(tg.cpu().numpy(), np.concatenate([t.reshape(-1) for t in tgs]),
+                 what="type grads")
+
+
+def test_vector_type_radii_required_when_type_indexed(vdata):
+    from paper_1912_04822_b200 import ConfigError, GridMaker
+
+    exs, ds = vdata
+    with pytest.raises(ConfigError, match="type_radii is missing"):
+        ds.batch(4).assemble(GridMaker(radius_type_indexed=True), [0, 17, 18])
