@@ -73,6 +73,13 @@ namespace {
 #ifndef GM_FWD_ZPLACE
 #define GM_FWD_ZPLACE 0  // zero groups in the job table: 0 spread evenly, 1 first, 2 last
 #endif
+#ifndef GM_FWD_TMA_ITEMS
+// 1: the cull's item records staged in shared memory by TMA bulk copies (one
+// lane, mbarrier-completed, next chunk in flight) instead of register
+// prefetch.  Bit-identical; measured 10 % slower (C2 forward 108.6 -> 119.5
+// us): the 2 KB stage per warp costs two resident CTAs per SM.
+#define GM_FWD_TMA_ITEMS 0
+#endif
 #ifndef GM_FWD_BUDGET_KB
 #define GM_FWD_BUDGET_KB 10
 #endif
@@ -195,15 +202,51 @@ __device__ __forceinline__ bool plan_visit(const FwdItem &it, int i, int jg0, in
 // Phases A/B of one warp region: the channel's items [cs, ce) scattered, in
 // order, into plane i, rows [jg0, jg1] of the accumulator (accp: plane i of
 // the tile, row j at (j - j0) * D).
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bar), "r"(phase)
+            : "memory");
+}
+
+// One lane stages items [from, from + n) (64 B each, contiguous) into shared
+// memory with a TMA bulk copy completing on mbarrier `bar`.
+__device__ __forceinline__ void stage_items(const FwdItem *src, FwdItem *dst, int n, uint32_t bar) {
+    const uint32_t bytes = (uint32_t)n * (uint32_t)sizeof(FwdItem);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
 template <bool BINARY, bool VECTOR, bool RESL>
 __device__ __forceinline__ void scatter_items(const FwdArgs &A, float *accp, Slot *slots, int lane,
                                               int e, int i, int jg0, int jg1, int j0, int cs,
-                                              int ce) {
+                                              int ce, FwdItem *stage, uint64_t *barp) {
     const int D = A.D;
     const double res = A.res;
     const float resf = A.resf, resl = A.resl, inv_res = A.inv_res;
     const double ox = A.origins[3 * e + 0], oy = A.origins[3 * e + 1],
                  oz = A.origins[3 * e + 2];
+#if GM_FWD_TMA_ITEMS
+    // the channel's item records arrive 32 at a time in shared memory by TMA
+    // bulk copies (one lane issues; the next chunk's copy is in flight while
+    // the current chunk scatters)
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(barp);
+    uint32_t phase = 0;
+    if (lane == 0 && cs < ce) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        stage_items(A.sorted + cs, stage, min(32, ce - cs), bar);
+    }
+    __syncwarp();
+#else
     // the next chunk's records are prefetched into registers while the
     // current chunk scatters (hides the L2 latency of phase A)
     FwdItem nxt;
@@ -212,9 +255,26 @@ __device__ __forceinline__ void scatter_items(const FwdArgs &A, float *accp, Slo
         nbox = A.sbox[cs + lane];
         nxt = A.sorted[cs + lane];
     }
+#endif
     for (int base = cs; base < ce; base += 32) {
         // ---- phase A: lane t plans item base + t ----
         const int it = base + lane;
+#if GM_FWD_TMA_ITEMS
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        FwdItem cur_item;
+        int2 bx = make_int2(1, 0);
+        if (it < ce) {
+            cur_item = stage[lane];
+            bx = make_int2(cur_item.ibox, cur_item.jbox);
+        }
+        __syncwarp();
+        if (lane == 0 && base + 32 < ce) {
+            // every lane has read the stage: reuse it for the next chunk
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            stage_items(A.sorted + base + 32, stage, min(32, ce - base - 32), bar);
+        }
+#else
         const FwdItem cur_item = nxt;
         const int2 bx = nbox;
         nbox = make_int2(1, 0);
@@ -222,6 +282,7 @@ __device__ __forceinline__ void scatter_items(const FwdArgs &A, float *accp, Slo
             nbox = A.sbox[it + 32];
             nxt = A.sorted[it + 32];
         }
+#endif
         bool hit = false;
         if (it < ce && box_lo(bx.x) <= i && box_hi(bx.x) >= i && box_lo(bx.y) <= jg1 &&
             box_hi(bx.y) >= jg0) {
@@ -455,7 +516,12 @@ __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs
                 for (int q = lane; q < nf; q += 32) rs[q] = 0.0f;
             }
         }
-        scatter_items<BINARY, VECTOR, RESL>(A, accp, slots, lane, e, i, jg0, jg1, j0, cs, ce);
+        FwdItem *stage = reinterpret_cast<FwdItem *>(smem + A.acc_floats * 4 +
+                                                     (size_t)kWarps * 32 * sizeof(Slot)) + warp * 32;
+        uint64_t *barp = reinterpret_cast<uint64_t *>(smem + A.acc_floats * 4 +
+                                                      (size_t)kWarps * 32 * (sizeof(Slot) + sizeof(FwdItem))) + warp;
+        scatter_items<BINARY, VECTOR, RESL>(A, accp, slots, lane, e, i, jg0, jg1, j0, cs, ce,
+                                            stage, barp);
     }
 
     // ---- the finished tile, zeros included ----
@@ -498,7 +564,8 @@ FwdConfig choose_config(int D) {
     cfg.TJ = std::min(TJ, D);
     cfg.rpw = (cfg.TJ + cfg.wpp - 1) / cfg.wpp;
     cfg.acc_floats = align_up((size_t)cfg.TI * cfg.TJ * D, 32);
-    cfg.smem = cfg.acc_floats * 4 + (size_t)kWarps * 32 * sizeof(Slot);
+    cfg.smem = cfg.acc_floats * 4 + (size_t)kWarps * 32 * sizeof(Slot) +
+               (GM_FWD_TMA_ITEMS ? (size_t)kWarps * (32 * sizeof(FwdItem) + 8) : 0);
     return cfg;
 }
 
