@@ -94,13 +94,13 @@ typedef struct {
      * one fully parallel pass. */
     const int32_t *item_perm;
     const int32_t *chan_off;
-    /* optional forward job table (device, 4 int32 per job: example, channel,
-     * tile, first plane | first row << 16), built by gm_forward_jobs
+    /* optional forward job table (device, 4 int32 per job: example | channel
+     * << 16, the channel's first and end item of the static grouping, first
+     * plane | first row << 16), built by gm_forward_jobs
      * from the static chan_off for grids of fwd_jobs_npts points per side: only
      * tiles of channels with items plus one job per group of zero tiles are
-     * launched (the kernel re-reads the item ranges of the prepare pass, so the
-     * table is valid after either prepare path).  NULL / 0 = one CTA per
-     * (channel, tile, example). */
+     * launched.  Used only with a static grouping (item_perm, chan_off), whose
+     * ranges the table carries.  NULL / 0 = one CTA per (channel, tile, example). */
     const int32_t *fwd_jobs;
     int32_t nfwd_jobs;
     int32_t fwd_jobs_npts;

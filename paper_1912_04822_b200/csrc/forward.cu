@@ -424,25 +424,28 @@ __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs
     const int D = A.D, TI = A.TI, TJ = A.TJ;
     if (A.jobs) {
         // job table: only tiles with items, one job per group of zero tiles;
-        // {example, channel, tile, first plane | first row << 16}: no integer
-        // division before the first load.  The item range is re-read from the
-        // prepare pass (a static channel with items may still lose them all
-        // to the grid's bounds).
+        // {example | channel << 16, first item, end item, first plane | first
+        // row << 16}: the channel's item range of the static grouping travels
+        // in the job (the prepare pass keeps every item of the grouping in
+        // place), so the first load is the items themselves -- no dependent
+        // chan_off load and no integer division before it
         const int4 j = A.jobs[blockIdx.x];
-        e = j.x;
-        c = j.y;
-        tile = j.z;
+        e = j.x & 0xffff;
+        c = (int)((unsigned)j.x >> 16);
+        cs = j.y;
+        ce = j.z;
         i0 = j.w & 0xffff;
         j0 = j.w >> 16;
+        tile = -1;  // derived below where needed (zero groups)
     } else {
         tile = blockIdx.y;
         e = blockIdx.z;
         c = blockIdx.x;
         i0 = (tile / A.ntj) * TI;
         j0 = (tile % A.ntj) * TJ;
+        cs = A.chan_off[(size_t)e * (A.C + 1) + c];
+        ce = A.chan_off[(size_t)e * (A.C + 1) + c + 1];
     }
-    cs = A.chan_off[(size_t)e * (A.C + 1) + c];
-    ce = A.chan_off[(size_t)e * (A.C + 1) + c + 1];
     const int TIv = min(TI, D - i0), TJv = min(TJ, D - j0);
     const size_t plane = (size_t)D * D;
     float *obase = A.out + ((size_t)e * A.C + c) * D * plane + (size_t)i0 * plane + (size_t)j0 * D;
@@ -453,6 +456,7 @@ __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs
         // Every GM_FWD_ZGROUP-th CTA of the slab writes its group of tiles
         // (contiguous in memory); the other CTAs of the group leave at once
         // (the job table does not even launch them).
+        if (tile < 0) tile = (i0 / TI) * A.ntj + j0 / TJ;
         if (tile % GM_FWD_ZGROUP) return;
         const int t1 = min(tile + GM_FWD_ZGROUP, A.ntiles);
         const int i1 = (t1 - 1) / A.ntj * TI, jl = ((t1 - 1) % A.ntj) * TJ;
@@ -673,8 +677,8 @@ __device__ __forceinline__ long long zeros_before(long long k, const JobGeom &J)
 }
 
 // One thread per (group, tile): the job's final slot.
-__global__ void __launch_bounds__(256) k_job_place(int nex, int nch, const int4 *stats,
-                                                   int4 *jobs, const JobGeom J) {
+__global__ void __launch_bounds__(256) k_job_place(const int32_t *co, int nex, int nch,
+                                                   const int4 *stats, int4 *jobs, const JobGeom J) {
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (long long)nex * nch * J.ntiles) return;
     const int g = (int)(idx / J.ntiles), t = (int)(idx - (long long)g * J.ntiles);
@@ -712,7 +716,8 @@ __global__ void __launch_bounds__(256) k_job_place(int nex, int nch, const int4 
         const long long zi = nzt * s0.y + (long long)(t / GM_FWD_ZGROUP) * s0.z + s0.w;
         k = ((zi + 1) * J.n + J.Z - 1) / J.Z - 1;  // ceil((zi + 1) n / Z) - 1
     }
-    jobs[k] = make_int4(e, c, t, ((t / J.ntj) * J.TI) | (((t % J.ntj) * J.TJ) << 16));
+    jobs[k] = make_int4(e | (c << 16), co[e * (nch + 1) + c], co[e * (nch + 1) + c + 1],
+                        ((t / J.ntj) * J.TI) | (((t % J.ntj) * J.TJ) << 16));
 }
 
 }  // namespace
@@ -749,7 +754,7 @@ gm_status forward_jobs_device(const gm_params *p, int nex, int nch, const int32_
     k_job_stats<<<(G + 7) / 8, 256, 0, s>>>(chan_off, nex, nch, stats);
     LAUNCH_CHECK();
     const long long nt = (long long)G * J.ntiles;
-    k_job_place<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(nex, nch, stats,
+    k_job_place<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(chan_off, nex, nch, stats,
                                                             reinterpret_cast<int4 *>(jobs), J);
     LAUNCH_CHECK();
     return GM_OK;
@@ -785,7 +790,9 @@ gm_status forward_impl(const gm_params *p, const gm_batch *b, const Workspace &w
     A.bulk = (D % 4) == 0 && ((uintptr_t)out % 16) == 0;
     A.acc_floats = cfg.acc_floats;
     A.ntiles = ((D + cfg.TI - 1) / cfg.TI) * A.ntj;
-    const bool jobs = b->fwd_jobs && b->fwd_jobs_npts == D && b->nfwd_jobs >= 0;
+    // the job table carries the static grouping's item ranges: only with one
+    const bool jobs = b->fwd_jobs && b->fwd_jobs_npts == D && b->nfwd_jobs >= 0 &&
+                      b->item_perm && b->chan_off;
     A.jobs = jobs ? reinterpret_cast<const int4 *>(b->fwd_jobs) : nullptr;
     const int nj = jobs ? b->nfwd_jobs : 0;
     if (p->binary)
@@ -822,7 +829,8 @@ int32_t forward_jobs_impl(const gm_params *p, int32_t nex, int32_t nch, const in
                 }
             }
     const long long n = (long long)work.size() + (long long)zero.size();
-    if (n > 0x7fffffffLL || D > 0x7fff) return -1;  // plane | row << 16 must fit
+    if (n > 0x7fffffffLL || D > 0x7fff || nex > 0xffff || nch > 0x7fff)
+        return -1;  // example | channel << 16 and plane | row << 16 must fit
     if (jobs && D <= GM_FWD_LPT_MAXD) {
 #if GM_FWD_LPT
         // heaviest first within groups of GM_FWD_LPT_GROUP examples (0: globally)
@@ -868,9 +876,9 @@ int32_t forward_jobs_impl(const gm_params *p, int32_t nex, int32_t nch, const in
 #endif
             const Job &j = z ? zero[zi++] : work[wi++];
             int32_t *o = jobs + 4 * k;
-            o[0] = j.slab / nch;  // example
-            o[1] = j.slab % nch;  // channel
-            o[2] = j.tile;
+            o[0] = (j.slab / nch) | ((j.slab % nch) << 16);  // example | channel << 16
+            o[1] = j.cs;                                     // the channel's item range
+            o[2] = j.ce;
             o[3] = ((j.tile / ntj) * cfg.TI) | (((j.tile % ntj) * cfg.TJ) << 16);
         }
     }

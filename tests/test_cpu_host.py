@@ -358,9 +358,18 @@ def test_forward_job_table_covers_every_tile_once():
         assert pb.nsegs == int((np.diff(co2, axis=1) > 0).sum())
         nonzero = {(e, c) for e in range(3) for c in range(28) if co2[e, c + 1] > co2[e, c]}
         seen = {}
-        for e, c, t, ij in jobs:
-            seen.setdefault((e, c), []).append(t)
-            assert 0 <= ij & 0xffff < D and 0 <= ij >> 16 < D
+        ntj = None
+        for ec, cs, ce, ij in jobs:
+            e, c = ec & 0xffff, ec >> 16
+            i0, j0 = ij & 0xffff, ij >> 16
+            assert 0 <= i0 < D and 0 <= j0 < D
+            assert (cs, ce) == (co2[e, c], co2[e, c + 1])  # the static item range
+            seen.setdefault((e, c), []).append((i0, j0))
+        # tiles as (plane, row band) pairs -> dense tile indices
+        rows = sorted({j for v in seen.values() for (_, j) in v})
+        planes = sorted({i for v in seen.values() for (i, _) in v})
+        ntj = len(rows)
+        seen = {k: [planes.index(i) * ntj + rows.index(j) for (i, j) in v] for k, v in seen.items()}
         ntiles = max(max(v) for v in seen.values()) + 1
         for (e, c), ts in seen.items():
             if (e, c) in nonzero:

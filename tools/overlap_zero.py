@@ -34,7 +34,7 @@ for pb in pbs:
     jobs = pb._jobs.cpu().numpy()
     off = pb.offsets["chan_off"][0]
     co = pb.host.numpy()[off:off + 4 * N * (C + 1)].view(np.int32).reshape(N, C + 1)
-    cnt = co[jobs[:, 0], jobs[:, 1] + 1] - co[jobs[:, 0], jobs[:, 1]]
+    cnt = jobs[:, 2] - jobs[:, 1]  # job: example | channel << 16, item range, plane | row << 16
     work = torch.from_numpy(np.ascontiguousarray(jobs[cnt > 0])).cuda()
     zero = torch.from_numpy(np.ascontiguousarray(jobs[cnt == 0])).cuda()
     parts.append({"all": (pb._jobs, pb._jobs.shape[0]), "work": (work, work.shape[0]),
