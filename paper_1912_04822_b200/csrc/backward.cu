@@ -37,6 +37,7 @@ struct BwdArgs {
     double *type_grad64;   // points return the f64 sums like _kernels.py:214,265)
     const BwdAtom *batoms; // index mode: per-atom records of the prepare pass
     const int32_t *atom_order; // vector mode: atom of each launch slot (bwd_slot inverse)
+    const VBwdAtom *vbatoms;   // vector mode: per-slot records of the prepare pass
     double eg;             // exp(-2 grm^2), a batch constant (_kernels.py:224)
     int early;             // 1: the records may be read before the PDL wait (the
                            // previous launch on this workspace was the forward)
@@ -46,6 +47,7 @@ struct BwdArgs {
 // One atom (for one channel radius): position, origin, full voxel box.
 struct Atom {
     double x, y, z, ox, oy, oz;
+    double r;  // radius * radius_scale (vector walk)
     double dzr, dzr2, m2inv_r2;
     int i0, i1, j0, j1, k0, k1;
 };
@@ -110,18 +112,6 @@ __device__ __forceinline__ double widen(float f) {
 // floor(a / b) for 0 <= a < 2^16, 1 <= b <= 64 (float reciprocal, exact here).
 __device__ __forceinline__ int idiv(int a, float inv_b) {
     return (int)(((float)a + 0.5f) * inv_b);
-}
-
-__device__ __forceinline__ void load_atom(const BwdArgs &P, int a, Atom &A, int &s, int &e) {
-    const gm_batch &b = P.b;
-    s = b.atom_set[a];
-    e = b.set_example[s];
-    A.x = P.pos[3 * a];
-    A.y = P.pos[3 * a + 1];
-    A.z = P.pos[3 * a + 2];
-    A.ox = b.origins[3 * e];
-    A.oy = b.origins[3 * e + 1];
-    A.oz = b.origins[3 * e + 2];
 }
 
 // Box for cutoff rmult*r (_kernels.py:225-227); false when it misses the grid.
@@ -574,7 +564,7 @@ __device__ __forceinline__ void vector_shared_walk(const BwdArgs &P, WarpBwd &W,
     constexpr int NC = NT > 0 ? NT : kMaxT;
     const gm_batch &b = P.b;
     const double grm = P.p.gaussian_radius_multiple, rmult = P.p.radius_multiple;
-    const double r = b.atom_radius[a];
+    const double r = A.r;
     const double gr = grm * r, d02 = gr * gr;
     const double q0 = (2.0 * grm) / r;
     const double qa = P.eg * (q0 * q0);
@@ -677,19 +667,26 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWDV_MINB) k_backward_vecto
     const int slot = blockIdx.x * kBwdWarps + warp;
     const gm_batch &b = P.b;
     if (slot >= b.natoms) return;
-    // heaviest atoms first when the batch carries a launch order (bwd_slot)
-    const int a = b.bwd_slot ? P.atom_order[slot] : slot;
+    // the prepare pass's record at this launch slot (heaviest atoms first when
+    // the batch carries a launch order): one load level
+    const VBwdAtom V = P.vbatoms[slot];
+    const int a = V.atom, s = V.set;
     const int D = P.p.npts;
     const double res = P.p.resolution, grm = P.p.gaussian_radius_multiple,
                  rmult = P.p.radius_multiple;
     const float inv_res = (float)(1.0 / res);
     Atom A;
-    int s, e;
-    load_atom(P, a, A, s, e);
-    const int Tn = b.set_t[s];
-    const int row = b.set_wstart[s] + (a - b.set_start[s]) * Tn;
+    A.x = V.x;
+    A.y = V.y;
+    A.z = V.z;
+    A.ox = V.ox;
+    A.oy = V.oy;
+    A.oz = V.oz;
+    A.r = V.r;
+    const int Tn = V.T;
+    const int row = V.row;
     const size_t D3 = (size_t)D * D * D;
-    const float *gset = P.grid_grad + ((size_t)e * b.nchannels + b.set_choff[s]) * D3;
+    const float *gset = P.grid_grad + (size_t)V.slab * D3;
     double gx = 0.0, gy = 0.0, gz = 0.0;
 
     if (!P.p.radius_type_indexed && Tn <= kMaxT) {
@@ -704,7 +701,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWDV_MINB) k_backward_vecto
     } else {
         for (int c = 0; c < Tn; c++) {
             const double r = P.p.radius_type_indexed ? b.type_radius[b.set_trstart[s] + c]
-                                                     : b.atom_radius[a];
+                                                     : A.r;
             const double w = (double)b.weights[row + c];
             const double gr = grm * r, d02 = gr * gr;
             const double q0 = (2.0 * grm) / r;
@@ -763,6 +760,7 @@ gm_status backward_impl(const gm_params *p, const gm_batch *b, const Workspace &
     P.type_grad = type_grad;
     P.batoms = ws.batoms;
     P.atom_order = ws.atom_order;
+    P.vbatoms = ws.vbatoms;
     P.eg = exp((-2.0 * p->gaussian_radius_multiple) * p->gaussian_radius_multiple);
     if (b->vector_mode)
         k_backward_vector<<<(b->natoms + kBwdWarps - 1) / kBwdWarps, kBwdWarps * 32, 0, s>>>(P);

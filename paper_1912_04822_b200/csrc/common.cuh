@@ -73,6 +73,21 @@ struct __align__(16) BwdAtom {
 };
 static_assert(sizeof(BwdAtom) == 96, "BwdAtom must be 96 bytes");
 
+// Vector-mode backward record of one atom, at its launch slot: everything
+// the walk needs in one load level (instead of atom -> set -> example chains).
+struct __align__(16) VBwdAtom {
+    double x, y, z;          // transformed position
+    double ox, oy, oz;       // the example's origin
+    double r;                // radius * radius_scale
+    int atom;                // packed atom index
+    int slab;                // e * nchannels + set_choff: the set's first grid_grad slab
+    int row;                 // first entry of the atom's weight row
+    int T;                   // the set's channel count
+    int set;                 // packed set index
+    int pad;
+};
+static_assert(sizeof(VBwdAtom) == 80, "VBwdAtom must be 80 bytes");
+
 __host__ __device__ inline int box_lo(int b) { return b & 0xffff; }
 __host__ __device__ inline int box_hi(int b) { return b >> 16; }
 
@@ -114,6 +129,7 @@ struct Workspace {
     BinItem *pbsorted;   // nitems (binary mode)
     int32_t *poff;       // nexamples * nchannels * kPlaneRec: plane-bucket offsets + max width
     int32_t *atom_order; // natoms (vector mode with gm_batch.bwd_slot): atom of each launch slot
+    VBwdAtom *vbatoms;   // natoms (vector mode): backward records at launch slots
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -144,6 +160,7 @@ inline size_t carve_workspace(void *base, int32_t natoms, int32_t nitems, int32_
     ws->pbsorted = (BinItem *)take(sizeof(BinItem) * ni);
     ws->poff = (int32_t *)take(sizeof(int32_t) * (size_t)std::max(nex, 1) * std::max(nch, 1) * kPlaneRec);
     ws->atom_order = (int32_t *)take(sizeof(int32_t) * na);
+    ws->vbatoms = (VBwdAtom *)take(sizeof(VBwdAtom) * na);
     return off + 256;
 }
 

@@ -97,6 +97,28 @@ __device__ __forceinline__ void store_pos(const PrepArgs &A, int a, const double
     A.ws.pos[3 * a + 2] = x[2];
 }
 
+// Vector mode: the backward's per-atom record at its launch slot.
+__device__ __forceinline__ void store_vbwd_atom(const PrepArgs &A, int a, int s, int e,
+                                                const double *O, const double x[3], int slot) {
+    const gm_batch &b = A.b;
+    if (!b.set_wstart) return;  // no weight rows: the batch has no vector backward
+    VBwdAtom v;
+    v.x = x[0];
+    v.y = x[1];
+    v.z = x[2];
+    v.ox = O[0];
+    v.oy = O[1];
+    v.oz = O[2];
+    v.r = b.atom_radius[a];
+    v.atom = a;
+    v.slab = e * b.nchannels + b.set_choff[s];
+    v.T = b.set_t[s];
+    v.row = b.set_wstart[s] + (a - b.set_start[s]) * v.T;
+    v.set = s;
+    v.pad = 0;
+    A.ws.vbatoms[slot] = v;
+}
+
 // Positions only (the vector-mode backward needs every atom, with or without
 // items).
 __global__ void __launch_bounds__(256) k_prepare_atoms(const PrepArgs A) {
@@ -105,7 +127,12 @@ __global__ void __launch_bounds__(256) k_prepare_atoms(const PrepArgs A) {
         double x[3];
         transform_atom(A, a, x);
         store_pos(A, a, x);
-        if (A.b.vector_mode && A.b.bwd_slot) A.ws.atom_order[A.b.bwd_slot[a]] = a;
+        if (A.b.vector_mode) {
+            const int slot = A.b.bwd_slot ? A.b.bwd_slot[a] : a;
+            if (A.b.bwd_slot) A.ws.atom_order[slot] = a;
+            const int st = A.b.atom_set[a], ex = A.b.set_example[st];
+            store_vbwd_atom(A, a, st, ex, A.b.origins + 3 * (size_t)ex, x, slot);
+        }
     }
 }
 
@@ -334,7 +361,9 @@ __global__ void __launch_bounds__(GM_PREP_THREADS) k_prepare_static(const PrepAr
         double x[3];
         transform_atom_x(A, t, s, xf ? xf + 15 * e : nullptr, x);
         store_pos(A, t, x);
-        if (b.bwd_slot) A.ws.atom_order[b.bwd_slot[t]] = t;  // vector backward launch order
+        const int slot = b.bwd_slot ? b.bwd_slot[t] : t;
+        if (b.bwd_slot) A.ws.atom_order[slot] = t;  // vector backward launch order
+        store_vbwd_atom(A, t, s, e, org + 3 * e, x, slot);
     }
     if (t < b.nitems) {
         FwdItem f;
@@ -427,7 +456,10 @@ __global__ void __launch_bounds__(1024) k_prepare_example(const PrepArgs A) {
             double x[3];
             transform_atom(A, a, x);
             store_pos(A, a, x);
-            if (b.bwd_slot) A.ws.atom_order[b.bwd_slot[a]] = a;
+            const int slot = b.bwd_slot ? b.bwd_slot[a] : a;
+            if (b.bwd_slot) A.ws.atom_order[slot] = a;
+            const int st = b.atom_set[a], ex = b.set_example[st];
+            store_vbwd_atom(A, a, st, ex, b.origins + 3 * (size_t)ex, x, slot);
         }
     }
     for (int q = threadIdx.x; q < n; q += blockDim.x) {
