@@ -501,10 +501,20 @@ __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs
     if (A.poff) {
         // items sorted by first plane (k_sort_planes): only those whose first
         // plane lies within the channel's widest box of plane i can reach it
+        // the channel's bucket record read by the warp in one load level
+        // (lanes hold entries lane, lane + 32, lane + 64), picked by shuffles
+        static_assert(kPlaneRec <= 96 && kBuckets == 64, "bucket record layout");
         const int32_t *rec = A.poff + ((size_t)e * A.C + c) * kPlaneRec;
-        const int wmax = rec[kBuckets + 2];
+        const int v0 = rec[lane], v1 = rec[32 + lane];
+        const int v2 = lane < kPlaneRec - 64 ? rec[64 + lane] : 0;
+        auto pick = [&](int k) {
+            const int a0 = __shfl_sync(0xffffffffu, v0, k & 31), a1 = __shfl_sync(0xffffffffu, v1, k & 31),
+                      a2 = __shfl_sync(0xffffffffu, v2, k & 31);
+            return k < 32 ? a0 : (k < 64 ? a1 : a2);
+        };
+        const int wmax = pick(kBuckets + 2);
         const int b0 = plane_bucket(max(0, i - wmax + 1), D), b1 = plane_bucket(min(i, D - 1), D);
-        const int rs = rec[b0], re = rec[b1 + 1];
+        const int rs = pick(b0), re = pick(b1 + 1);
         ce = cs + re;
         cs = cs + rs;
     }
