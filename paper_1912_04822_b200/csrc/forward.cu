@@ -413,8 +413,11 @@ template <bool BINARY, bool VECTOR, bool RESL>
 __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs A) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // the prepare pass's records must be complete; then the backward (next in
-    // the stream) may begin its prologue while this grid drains
+    // the job (built before the prepare pass, complete when it started) is
+    // read before the wait; the prepare pass's records must be complete
+    // before anything else, then the backward (next in the stream) may begin
+    // its prologue while this grid drains
+    const int4 job = A.jobs ? A.jobs[blockIdx.x] : make_int4(0, 0, 0, 0);
     pdl_wait();
     pdl_trigger();
     // grid (channel, tile, example): consecutive CTAs are the channels of one
@@ -429,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs
         // in the job (the prepare pass keeps every item of the grouping in
         // place), so the first load is the items themselves -- no dependent
         // chan_off load and no integer division before it
-        const int4 j = A.jobs[blockIdx.x];
+        const int4 j = job;
         e = j.x & 0xffff;
         c = (int)((unsigned)j.x >> 16);
         cs = j.y;
