@@ -77,6 +77,15 @@ class GraphStep:
         self._done = [None, None]
         self._k = 0
         self._params = gm._gm_params(npts)
+        if self.augment and (self._params.matmul_order_1 < 0 or self._params.matmul_order_n < 0):
+            import warnings
+
+            # the captured prepare pass transforms on the device; the eager path
+            # falls back to host-transformed positions instead (voxelizer._prepare)
+            warnings.warn("numpy's float64 matmul rounding could not be calibrated on this "
+                          "host: the graph-captured transform may differ from numpy's in the "
+                          "last bit (binary occupancy is then not guaranteed bit-exact)",
+                          RuntimeWarning, stacklevel=2)
         pb.ensure_call_buffer(self.augment)
         self._batch = pb.gm_batch()
         self._origin_shift = float(gm.dimension) / 2.0
