@@ -48,12 +48,14 @@ def _dev_array(ab, name, n):
     return ab.dev[off:off + n * np.dtype(dt).itemsize].cpu().numpy().view(dt)
 
 
-@pytest.mark.parametrize("seed", [0, 1])
-def test_assembled_batch_equals_host_packing(data, seed):
+@pytest.mark.parametrize("seed,cfg", [(0, dict()), (1, dict()),
+                                      (2, dict(resolution=0.25, dimension=23.75)),
+                                      (3, dict(resolution=0.375, dimension=11.3, radius_scale=0.8))])
+def test_assembled_batch_equals_host_packing(data, seed, cfg):
     from paper_1912_04822_b200 import GridMaker, _native
 
     exs, ds = data
-    gm = GridMaker()
+    gm = GridMaker(**cfg)
     ids = np.random.default_rng(seed).permutation(len(exs))[:37]
     ab = ds.batch(50).assemble(gm, ids)
     pb = gm.pack([exs[i] for i in ids])
@@ -78,7 +80,7 @@ def test_assembled_batch_equals_host_packing(data, seed):
     bs = _dev_array(ab, "bwd_slot", A)
     assert np.array_equal(np.sort(bs), np.arange(A))
     # forward job table == the host builder's
-    p = gm._gm_params(48)
+    p = gm._gm_params(gm.points_per_side())
     co = np.ascontiguousarray(_host_array(pb, "chan_off", N * (C + 1)))
     L = _native.lib()
     cnt = L.gm_forward_jobs(ctypes.byref(p), N, C, co.ctypes.data, None, 0)
@@ -88,7 +90,9 @@ def test_assembled_batch_equals_host_packing(data, seed):
     np.testing.assert_array_equal(ab._jobs[:cnt].cpu().numpy(), jobs)
 
 
-@pytest.mark.parametrize("cfg", [dict(), dict(binary=True), dict(resolution=0.25, dimension=23.75)])
+@pytest.mark.parametrize("cfg", [dict(), dict(binary=True), dict(resolution=0.25, dimension=23.75),
+                                 dict(resolution=0.375, dimension=11.3),
+                                 dict(resolution=0.25, dimension=6.0, radius_scale=1.3)])
 def test_assembled_forward_backward_bitwise_and_vs_oracle(data, cfg):
     from paper_1912_04822_b200 import GridMaker, geom
 
