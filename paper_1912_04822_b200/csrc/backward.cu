@@ -177,6 +177,9 @@ constexpr int kBwdWarps = GM_BWD_WARPS;
 #ifndef GM_BWD_CHAINS
 #define GM_BWD_CHAINS 1
 #endif
+#ifndef GM_BWD_P1X2
+#define GM_BWD_P1X2 2  // index walk, phase 1: rows per lane per pass (1 or 2)
+#endif
 #ifndef GM_BWD_PREFETCH
 #define GM_BWD_PREFETCH 1  // L2 prefetch of each row span in phase 1 (C5 438 -> 424 us)
 #endif
@@ -449,53 +452,76 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
                         const int nwords = ((rend - rb) * nk + 31) >> 5;
                         for (int w = lane; w < nwords + kU; w += 32) W.starts[w] = 0u;
                         __syncwarp();
-                        for (int r0 = rb; r0 < rend; r0 += 32) {
-                            const int row = r0 + lane;
-                            int len = 0, klo = 0;
-                            const int ii = idiv(row, inv_nj), jj = row - ii * nj;
-                            double dx = 0.0, dy = 0.0, b2 = 0.0;
+                        // rows r0 + lane and (GM_BWD_P1X2) r0 + 32 + lane per pass:
+                        // two independent span / scan chains in flight
+                        struct Span {
+                            int len, klo, ii, jj;
+                            double dx, dy, b2;
+                        };
+                        auto span_of = [&](int row) {
+                            Span q{0, 0, 0, 0, 0.0, 0.0, 0.0};
+                            q.ii = idiv(row, inv_nj);
+                            q.jj = row - q.ii * nj;
                             if (row < rend) {
-                                dx = W.dx[ii];
-                                dy = W.dy[jj];
-                                b2 = fma(dy, dy, dx * dx);
-                                const double rem = dzr2 - b2;
+                                q.dx = W.dx[q.ii];
+                                q.dy = W.dy[q.jj];
+                                q.b2 = fma(q.dy, q.dy, q.dx * q.dx);
+                                const double rem = dzr2 - q.b2;
                                 if (rem > 0.0) {
                                     const float rho = fmaf(approx_sqrt((float)rem), 1.0001f,
                                                            1e-5f * (float)dzr);
-                                    klo = max(0, __float2int_ru(fmaxf((dz0 - rho) * inv_res, -1.0f)));
+                                    q.klo = max(0, __float2int_ru(fmaxf((dz0 - rho) * inv_res, -1.0f)));
                                     const int khi = min(nk - 1, __float2int_rd(fminf(
                                                                     (dz0 + rho) * inv_res, (float)nk)));
-                                    len = max(0, khi - klo + 1);
+                                    q.len = max(0, khi - q.klo + 1);
                                 }
                             }
-                            int sc = len;  // inclusive scan of the span lengths
+                            return q;
+                        };
+                        auto place = [&](const Span &q, int rowidx, int st) {
+                            IRow &R = W.rows[rowidx];
+                            atomicOr(&W.starts[st >> 5], 1u << (st & 31));
+                            R.dx = q.dx;
+                            R.dy = q.dy;
+                            R.b2 = q.b2;
+                            R.exy = (W.ex[q.ii] * W.ey[q.jj]) * B.m4inv_r2;
+                            R.gp = gbase + (sbase + (unsigned)((q.ii * D + q.jj) * D + q.klo)) - st;
+                            R.kz = q.klo - st;
+#if GM_BWD_PREFETCH
+                            // the row's grid_grad span into L2 now: phase 2's
+                            // loads then hit (a hint only, no ordering)
+                            const float *rp = R.gp + st;
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(rp));
+                            if ((((uintptr_t)rp) & 127u) + 4u * (unsigned)q.len > 128u)
+                                asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + q.len - 1));
+#endif
+                        };
+                        for (int r0 = rb; r0 < rend; r0 += 32 * GM_BWD_P1X2) {
+                            const Span qa = span_of(r0 + lane);
+                            Span qb{0, 0, 0, 0, 0.0, 0.0, 0.0};
+                            if (GM_BWD_P1X2 > 1) qb = span_of(r0 + 32 + lane);
+                            int sa = qa.len, sb = qb.len;  // inclusive scans of the span lengths
 #pragma unroll
                             for (int o = 1; o < 32; o <<= 1) {
-                                const int t = __shfl_up_sync(0xffffffffu, sc, o);
-                                if (lane >= o) sc += t;
+                                const int ta = __shfl_up_sync(0xffffffffu, sa, o);
+                                const int tb = GM_BWD_P1X2 > 1 ? __shfl_up_sync(0xffffffffu, sb, o) : 0;
+                                if (lane >= o) {
+                                    sa += ta;
+                                    sb += tb;
+                                }
                             }
-                            const unsigned m = __ballot_sync(0xffffffffu, len > 0);
-                            if (len > 0) {
-                                IRow &R = W.rows[nrow + __popc(m & lt)];
-                                const int st = total + sc - len;
-                                atomicOr(&W.starts[st >> 5], 1u << (st & 31));
-                                R.dx = dx;
-                                R.dy = dy;
-                                R.b2 = b2;
-                                R.exy = (W.ex[ii] * W.ey[jj]) * B.m4inv_r2;
-                                R.gp = gbase + (sbase + (unsigned)((ii * D + jj) * D + klo)) - st;
-                                R.kz = klo - st;
-#if GM_BWD_PREFETCH
-                                // the row's grid_grad span into L2 now: phase 2's
-                                // loads then hit (a hint only, no ordering)
-                                const float *rp = R.gp + st;
-                                asm volatile("prefetch.global.L2 [%0];" ::"l"(rp));
-                                if ((((uintptr_t)rp) & 127u) + 4u * (unsigned)len > 128u)
-                                    asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + len - 1));
-#endif
+                            const unsigned ma = __ballot_sync(0xffffffffu, qa.len > 0);
+                            const int tota = __shfl_sync(0xffffffffu, sa, 31);
+                            if (qa.len > 0) place(qa, nrow + __popc(ma & lt), total + sa - qa.len);
+                            nrow += __popc(ma);
+                            total += tota;
+                            if (GM_BWD_P1X2 > 1) {
+                                const unsigned mb = __ballot_sync(0xffffffffu, qb.len > 0);
+                                const int totb = __shfl_sync(0xffffffffu, sb, 31);
+                                if (qb.len > 0) place(qb, nrow + __popc(mb & lt), total + sb - qb.len);
+                                nrow += __popc(mb);
+                                total += totb;
                             }
-                            nrow += __popc(m);
-                            total += __shfl_sync(0xffffffffu, sc, 31);
                         }
                         __syncwarp();
                         // ---- phase 2: kU windows of 32 voxels per step ----
@@ -507,8 +533,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
                         // U windows from base; the loop's tail runs one window
                         // at a time (no clamped dead windows).  Lane l still
                         // visits voxels l, l+32, ... in order: same sums.
-                        auto step = [&](auto Uc, int base) {
+                        // FULL: every voxel of the U windows exists (no clamp, no mask)
+                        auto step = [&](auto Uc, auto Fc, int base) {
                             constexpr int U = decltype(Uc)::value;
+                            constexpr bool FULL = decltype(Fc)::value;
                             int myrow[U];
 #pragma unroll
                             for (int u = 0; u < U; u++) {
@@ -519,13 +547,13 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
                             float g[U];
 #pragma unroll
                             for (int u = 0; u < U; u++) {
-                                const int v = min(base + 32 * u + lane, last);
+                                const int v = FULL ? base + 32 * u + lane : min(base + 32 * u + lane, last);
                                 g[u] = ld_gg<GM_BWD_GGHINT>(W.rows[myrow[u]].gp + v);
                             }
 #pragma unroll
                             for (int u = 0; u < U; u++) {
                                 const int vr = base + 32 * u + lane;
-                                const int v = min(vr, last);
+                                const int v = FULL ? vr : min(vr, last);
                                 const IRow &R = W.rows[myrow[u]];
                                 const double2 zt = W.zt[R.kz + v];
                                 const double dz = zt.x;
@@ -535,7 +563,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
                                 // Ex Ey Ez (-4/r^2), tail 2 qa (d - dzr) / d; d2 = 0
                                 // takes the core branch and contributes 0 (dx=dy=dz=0)
                                 const double t = d2 <= d02 ? R.exy * zt.y : fma(-qa2dzr, rd, qa2);
-                                const double scl = (double)((vr <= last && d2 < dzr2) ? g[u] : 0.0f) * t;
+                                const double scl =
+                                    (double)(((FULL || vr <= last) && d2 < dzr2) ? g[u] : 0.0f) * t;
                                 gx = fma(scl, R.dx, gx);
                                 gy = fma(scl, R.dy, gy);
                                 gz = fma(scl, dz, gz);
@@ -543,8 +572,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
                         };
                         int base = 0;
                         for (; base + 32 * kU <= total; base += 32 * kU)
-                            step(std::integral_constant<int, kU>{}, base);
-                        for (; base < total; base += 32) step(std::integral_constant<int, 1>{}, base);
+                            step(std::integral_constant<int, kU>{}, std::true_type{}, base);
+                        for (; base < total; base += 32)
+                            step(std::integral_constant<int, 1>{}, std::false_type{}, base);
                         __syncwarp();
                     }
                 }
