@@ -589,7 +589,11 @@ def main():
                "note": "GridMaker.forward_packed/backward_packed with a pinned host->device "
                        "upload of the atoms each step (double-buffered on a copy stream, "
                        "overlapping the previous step's gridding), loss 1/2|grid|^2, "
-                       "coordinate gradients read back to pinned host memory"}
+                       "coordinate gradients read back to pinned host memory.  The SAME "
+                       "batch every step: its host packing happened once, outside the timed "
+                       "region (e2e_fresh packs a new batch every step, on the device), and "
+                       "the 620 MB of grids stay on the device as a CNN's input would "
+                       "(e2e_numpy returns them to the host)"}
 
     # ---- e2e_fresh: new, shuffled examples every step from a device-resident
     # dataset (DeviceDataset), each batch assembled on the device ----
