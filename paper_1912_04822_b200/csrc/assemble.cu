@@ -10,8 +10,8 @@
 // CTAs per (batch example, 256-atom chunk) copy its 32-B atom records into the packed
 // arrays the prepare pass reads (slot records in channel order, atoms in set
 // order), writes its set rows, channel offsets and nonzero-channel list.  The
-// forward job table follows on the device (forward.cu: k_job_stats /
-// k_job_place).  Batch sizes come from the dataset's host mirrors: no sync.
+// forward job table follows on the device (forward.cu: k_job_build).  Batch
+// sizes come from the dataset's host mirrors: no sync.
 #include "common.cuh"
 
 namespace {

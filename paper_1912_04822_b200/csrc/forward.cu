@@ -623,80 +623,16 @@ struct JobGeom {
     long long H;               // heavy slots of the dealing
 };
 
-// One warp per (example, channel) group: ranks of the group among all groups.
-// The group item counts are staged in shared memory first (the rank loop
-// then runs on shared-memory reads instead of serial L2 round trips).
-constexpr int kJobStatsMaxG = 12288;  // groups staged in shared memory (48 KB)
-__global__ void __launch_bounds__(256) k_job_stats(const int32_t *co, int nex, int nch,
-                                                   int4 *stats) {
-    __shared__ int cnt[kJobStatsMaxG];
-    const int G = nex * nch;
-    const bool staged = G <= kJobStatsMaxG;
-    if (staged)
-        for (int q = threadIdx.x; q < G; q += blockDim.x) {
-            const int e = q / nch, c = q - e * nch;
-            cnt[q] = co[e * (nch + 1) + c + 1] - co[e * (nch + 1) + c];
-        }
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int g = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (g >= G) return;
-    const int e = g / nch, c = g - e * nch;
-    auto count_of = [&](int q) {
-        if (staged) return cnt[q];
-        const int e2 = q / nch, c2 = q - e2 * nch;
-        return co[e2 * (nch + 1) + c2 + 1] - co[e2 * (nch + 1) + c2];
-    };
-    const int k0 = count_of(g);
-    int gt = 0, eqb = 0, eqe = 0, eqc = 0, nwb = 0, nwe = 0, nwc = 0;
-    const int gfirst = e * nch;  // first group of this example
-    for (int q = lane; q < G; q += 32) {
-        const int k = count_of(q);
-        const bool before = q < gfirst, same = q >= gfirst && q < gfirst + nch, cb = same && q < g;
-        if (k0 > 0) {
-            gt += k > k0;
-            eqb += k == k0 && before;
-            eqe += k == k0 && same;
-            eqc += k == k0 && cb;
-            nwb += k > 0 && before;
-            nwe += k > 0 && same;
-            nwc += k > 0 && cb;
-        } else {  // zero groups: rank among zero groups
-            eqb += k == 0 && before;
-            eqe += k == 0 && same;
-            eqc += k == 0 && cb;
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        gt += __shfl_xor_sync(0xffffffffu, gt, o);
-        eqb += __shfl_xor_sync(0xffffffffu, eqb, o);
-        eqe += __shfl_xor_sync(0xffffffffu, eqe, o);
-        eqc += __shfl_xor_sync(0xffffffffu, eqc, o);
-        nwb += __shfl_xor_sync(0xffffffffu, nwb, o);
-        nwe += __shfl_xor_sync(0xffffffffu, nwe, o);
-        nwc += __shfl_xor_sync(0xffffffffu, nwc, o);
-    }
-    if (lane == 0) {
-        stats[2 * g] = make_int4(gt, eqb, eqe, eqc);
-        stats[2 * g + 1] = make_int4(nwb, nwe, nwc, k0);
-    }
-}
-
 // zeros before table slot k: floor(k Z / n) (the host rule places zero job
 // zi at the first slot k with (zi + 1) n <= (k + 1) Z)
 __device__ __forceinline__ long long zeros_before(long long k, const JobGeom &J) {
     return J.Z ? (k * J.Z) / J.n : 0;
 }
 
-// One thread per (group, tile): the job's final slot.
-__global__ void __launch_bounds__(256) k_job_place(const int32_t *co, int nex, int nch,
-                                                   const int4 *stats, int4 *jobs, const JobGeom J) {
-    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (long long)nex * nch * J.ntiles) return;
-    const int g = (int)(idx / J.ntiles), t = (int)(idx - (long long)g * J.ntiles);
+// The final slot of group g's tile t.
+__device__ __forceinline__ void place_job(const int32_t *co, int nch, int g, int t, int4 s0,
+                                          int4 s1, int4 *jobs, const JobGeom &J) {
     const int e = g / nch, c = g - e * nch;
-    const int4 s0 = stats[2 * g], s1 = stats[2 * g + 1];
     long long k;
     if (s1.w > 0) {
         // rank in the sorted work list, then its slot in the heavy/light deal
@@ -733,6 +669,76 @@ __global__ void __launch_bounds__(256) k_job_place(const int32_t *co, int nex, i
                         ((t / J.ntj) * J.TI) | (((t % J.ntj) * J.TJ) << 16));
 }
 
+// One warp per (example, channel) group: ranks of the group among all groups.
+// The group item counts are staged in shared memory first (the rank loop
+// then runs on shared-memory reads instead of serial L2 round trips).
+constexpr int kJobStatsMaxG = 12032;  // groups staged in shared memory (static 48 KB with the stats)
+// CTA of 8 warps <-> 8 groups: each warp ranks its group, then the CTA places
+// the groups' jobs (one launch for the whole table)
+__global__ void __launch_bounds__(256) k_job_build(const int32_t *co, int nex, int nch,
+                                                   int4 *jobs, const JobGeom J) {
+    __shared__ int cnt[kJobStatsMaxG];
+    __shared__ int4 st[8][2];
+    const int G = nex * nch;
+    const bool staged = G <= kJobStatsMaxG;
+    if (staged)
+        for (int q = threadIdx.x; q < G; q += blockDim.x) {
+            const int e = q / nch, c = q - e * nch;
+            cnt[q] = co[e * (nch + 1) + c + 1] - co[e * (nch + 1) + c];
+        }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int g = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int e = g / nch, c = g - e * nch;
+    auto count_of = [&](int q) {
+        if (staged) return cnt[q];
+        const int e2 = q / nch, c2 = q - e2 * nch;
+        return co[e2 * (nch + 1) + c2 + 1] - co[e2 * (nch + 1) + c2];
+    };
+    const int k0 = g < G ? count_of(g) : 0;
+    int gt = 0, eqb = 0, eqe = 0, eqc = 0, nwb = 0, nwe = 0, nwc = 0;
+    const int gfirst = e * nch;  // first group of this example
+    for (int q = lane; q < (g < G ? G : 0); q += 32) {
+        const int k = count_of(q);
+        const bool before = q < gfirst, same = q >= gfirst && q < gfirst + nch, cb = same && q < g;
+        if (k0 > 0) {
+            gt += k > k0;
+            eqb += k == k0 && before;
+            eqe += k == k0 && same;
+            eqc += k == k0 && cb;
+            nwb += k > 0 && before;
+            nwe += k > 0 && same;
+            nwc += k > 0 && cb;
+        } else {  // zero groups: rank among zero groups
+            eqb += k == 0 && before;
+            eqe += k == 0 && same;
+            eqc += k == 0 && cb;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        gt += __shfl_xor_sync(0xffffffffu, gt, o);
+        eqb += __shfl_xor_sync(0xffffffffu, eqb, o);
+        eqe += __shfl_xor_sync(0xffffffffu, eqe, o);
+        eqc += __shfl_xor_sync(0xffffffffu, eqc, o);
+        nwb += __shfl_xor_sync(0xffffffffu, nwb, o);
+        nwe += __shfl_xor_sync(0xffffffffu, nwe, o);
+        nwc += __shfl_xor_sync(0xffffffffu, nwc, o);
+    }
+    if (lane == 0) {
+        st[threadIdx.x >> 5][0] = make_int4(gt, eqb, eqe, eqc);
+        st[threadIdx.x >> 5][1] = make_int4(nwb, nwe, nwc, k0);
+    }
+    __syncthreads();
+    // the CTA's groups' jobs: (group, tile) pairs, 256 threads at a time
+    const int g0 = blockIdx.x * 8, ng = min(8, G - g0);
+    for (int q = threadIdx.x; q < ng * J.ntiles; q += blockDim.x) {
+        const int gl = q / J.ntiles, t = q - gl * J.ntiles;
+        place_job(co, nch, g0 + gl, t, st[gl][0], st[gl][1], reinterpret_cast<int4 *>(jobs), J);
+    }
+}
+
+
 }  // namespace
 
 // Job count of a grid size for the given numbers of (example, channel) groups
@@ -764,11 +770,8 @@ gm_status forward_jobs_device(const gm_params *p, int nex, int nch, const int32_
     }
     const int G = nex * nch;
     if (G == 0 || J.n == 0) return GM_OK;
-    k_job_stats<<<(G + 7) / 8, 256, 0, s>>>(chan_off, nex, nch, stats);
-    LAUNCH_CHECK();
-    const long long nt = (long long)G * J.ntiles;
-    k_job_place<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(chan_off, nex, nch, stats,
-                                                            reinterpret_cast<int4 *>(jobs), J);
+    (void)stats;
+    k_job_build<<<(G + 7) / 8, 256, 0, s>>>(chan_off, nex, nch, reinterpret_cast<int4 *>(jobs), J);
     LAUNCH_CHECK();
     return GM_OK;
 }
