@@ -457,13 +457,19 @@ def _bwd_slots(coords, atom_example, centers, per_example=False, slab=None):
     # grid_grad slabs stay in L2: the vector backward reads every channel)
     per_example = per_example or _BWD_ORDER == "lpt_local"
     if per_example:
-        key = atom_example.astype(np.int64) * 32768 + key
-    elif _BWD_ORDER == "slab" and slab is not None:
+        slab = atom_example  # grouped by example, nearest first within it
+    if per_example or (_BWD_ORDER == "slab" and slab is not None):
         # the atoms of one (example, channel) grid_grad slab together, nearest
         # first: overlapping spheres re-read the slab from L2 (C5 DRAM reads
-        # 1152 -> 552 MB, 3.5x -> 1.7x the footprint; times unchanged)
-        key = slab.astype(np.int64) * 32768 + key
-    order = np.argsort(key, kind="stable")
+        # 1152 -> 552 MB, 3.5x -> 1.7x the footprint; times unchanged).  Two
+        # stable 16-bit sorts (numpy's radix sort) instead of one 64-bit sort.
+        order = np.argsort(key, kind="stable")
+        sl = slab[order]
+        sl = sl.astype(np.int16) if sl.size and int(sl.max()) < 32767 else sl
+        order = order[np.argsort(sl, kind="stable")]
+        key = None
+    if key is not None:
+        order = np.argsort(key, kind="stable")
     if _BWD_ORDER == "alt":
         alt = np.empty(n, np.int64)
         alt[0::2] = order[:(n + 1) // 2]

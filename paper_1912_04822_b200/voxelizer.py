@@ -230,6 +230,39 @@ class GridMaker:
                                bool(self.radius_type_indexed) and check_type_radii,
                                dev, centers=None)
 
+    def _pack_cached(self, example_sets, nchannels, device, check_type_radii=True) -> PackedBatch:
+        """``pack`` for the one-shot numpy API, reusing the last batch when the
+        same examples come back unchanged (``forward_batch`` followed by
+        ``backward_batch`` on the same examples packs once).  A hit needs the
+        same set objects AND equal coordinates, radii and types (checked on
+        concatenated copies, ~1 ms for C2 vs ~9 ms to pack)."""
+        sets = [cs for ss in example_sets for cs in ss]
+        key = (tuple(id(cs) for cs in sets), tuple(len(ss) for ss in example_sets),
+               int(nchannels), str(device), float(self.radius_scale),
+               bool(self.radius_type_indexed) and check_type_radii)
+
+        def snap():
+            cat = (lambda xs: np.concatenate(xs) if xs else np.zeros(0))
+            return (cat([np.asarray(cs.coords).reshape(-1) for cs in sets]),
+                    cat([np.asarray(cs.radii).reshape(-1) for cs in sets]),
+                    cat([np.asarray(cs.type_index).reshape(-1) for cs in sets
+                         if getattr(cs, "type_index", None) is not None]),
+                    cat([np.asarray(cs.type_vector).reshape(-1) for cs in sets
+                         if getattr(cs, "type_vector", None) is not None]),
+                    cat([np.asarray(cs.type_radii).reshape(-1) for cs in sets
+                         if getattr(cs, "type_radii", None) is not None]))
+
+        cached = self.__dict__.get("_pack_cache")
+        now = snap()
+        if cached is not None and cached[0] == key and len(cached[2]) == len(now) and \
+                all(a.shape == b.shape and np.array_equal(a, b) for a, b in zip(cached[2], now)):
+            return cached[1]
+        pb = self.pack(example_sets, nchannels=nchannels, device=device,
+                       check_type_radii=check_type_radii)
+        # the set objects are kept alive with the entry, so their ids stay theirs
+        self.__dict__["_pack_cache"] = (key, pb, now, sets)
+        return pb
+
     def _prepare(self, pb: PackedBatch, centers, transforms, npts) -> _native.GmParams:
         if centers is None:
             key = float(self.dimension)
@@ -449,7 +482,7 @@ class GridMaker:
             return (arr, None) if want_transforms else arr
         nch = shape[0] if single else shape[1]
         dev = arr.device if _is_tensor(arr) else self._device()
-        pb = self.pack(example_sets, nchannels=nch, device=dev)
+        pb = self._pack_cached(example_sets, nch, dev)
         dshape = (1,) + shape if single else shape
         if _is_tensor(arr):
             dout = arr.view(dshape)
@@ -528,8 +561,7 @@ class GridMaker:
             raise ValueError(f"grid_grad shape {tuple(gg.shape)} does not match {expected}")
         as_tensor = _is_tensor(gg)
         dev = gg.device if as_tensor else self._device()
-        pb = self.pack(example_sets, nchannels=nch, device=dev,
-                       check_type_radii=not self.binary)
+        pb = self._pack_cached(example_sets, nch, dev, check_type_radii=not self.binary)
         if as_tensor:
             dgg = gg.to(torch.float32).contiguous()
         else:

@@ -167,3 +167,34 @@ def test_grid_views_as_out_and_grid_grad(rng):
     out = np.zeros((1, 4, D, D, D), np.float32)
     gm.forward_batch([cs], out=Duck(out))
     assert_close(out[0], ref, what="duck-typed grid")
+
+
+def test_numpy_api_pack_cache_hits_and_invalidates(monkeypatch):
+    """forward_batch -> backward_batch on the same examples packs once; an
+    in-place coordinate change (same objects) repacks."""
+    import paper_1912_04822_b200.voxelizer as vz
+    from paper_1912_04822_b200 import GridMaker, synthetic
+
+    exs = synthetic.batch(3, seed=2)
+    gm = GridMaker()
+    calls = []
+    real = vz.PackedBatch
+
+    def counting(*a, **k):
+        calls.append(1)
+        return real(*a, **k)
+
+    monkeypatch.setattr(vz, "PackedBatch", counting)
+    g1, xf = gm.forward_batch(exs, random_rotation=True, random_translation=2.0,
+                              rng=np.random.default_rng(0), return_transforms=True)
+    res = gm.backward_batch(exs, g1, transforms=xf)
+    assert len(calls) == 1
+    go = oracle.GridOracle()
+    cgs, _ = go.backward_batch(exs, g1, random_rotation=True, random_translation=2.0,
+                               rng=np.random.default_rng(0))
+    assert_close(np.concatenate([c for ex in res for (c, _) in ex]), np.concatenate(cgs),
+                 what="cached-pack backward")
+    exs[1].coord_sets[0].coords[5] += np.float32(0.75)  # in place: same objects
+    g2 = gm.forward_batch(exs)
+    assert len(calls) == 2
+    assert_close(g2, go.forward_batch(exs), what="repacked after an in-place change")
