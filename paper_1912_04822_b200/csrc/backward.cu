@@ -181,7 +181,12 @@ constexpr int kBwdWarps = GM_BWD_WARPS;
 #define GM_BWD_P1X2 2  // index walk, phase 1: rows per lane per pass (1 or 2)
 #endif
 #ifndef GM_BWD_PREFETCH
-#define GM_BWD_PREFETCH 1  // L2 prefetch of each row span in phase 1 (C5 438 -> 424 us)
+// L2 prefetch of each row span in phase 1: 0 none, 1 prefetch.global.L2 of the
+// span's first / last line, 2 cp.async.bulk.prefetch of exactly its 16-B
+// granules.  C2 / C5 backward: 102.7 / 479.6 us, 94.5 / 436.6 us, 123.1 / 512.5
+// us; DRAM reads equal in all three (83.5 / 550 MB: HBM fills whole 128-B
+// lines, tools/pf_ab.sh)
+#define GM_BWD_PREFETCH 1
 #endif
 #ifndef GM_BWD_GGHINT
 #define GM_BWD_GGHINT 0  // cache hint of the index-mode grid_grad loads (see ld_gg)
@@ -487,13 +492,23 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
                             R.exy = (W.ex[q.ii] * W.ey[q.jj]) * B.m4inv_r2;
                             R.gp = gbase + (sbase + (unsigned)((q.ii * D + q.jj) * D + q.klo)) - st;
                             R.kz = q.klo - st;
-#if GM_BWD_PREFETCH
+#if GM_BWD_PREFETCH == 1
                             // the row's grid_grad span into L2 now: phase 2's
                             // loads then hit (a hint only, no ordering)
                             const float *rp = R.gp + st;
                             asm volatile("prefetch.global.L2 [%0];" ::"l"(rp));
                             if ((((uintptr_t)rp) & 127u) + 4u * (unsigned)q.len > 128u)
                                 asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + q.len - 1));
+#elif GM_BWD_PREFETCH == 2
+                            // the same as a bulk L2 prefetch of exactly the
+                            // span's 16-B granules (no whole-line fetches)
+                            {
+                                const uintptr_t p0 = (uintptr_t)(R.gp + st) & ~(uintptr_t)15;
+                                const uintptr_t p1 = ((uintptr_t)(R.gp + st + q.len) + 15) & ~(uintptr_t)15;
+                                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0),
+                                             "r"((unsigned)(p1 - p0))
+                                             : "memory");
+                            }
 #endif
                         };
                         for (int r0 = rb; r0 < rend; r0 += 32 * GM_BWD_P1X2) {

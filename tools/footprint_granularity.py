@@ -1,7 +1,12 @@
-"""C2 backward footprint at 4-B, 32-B, 64-B and 128-B granularity (first 6
-examples, untransformed): the DRAM-read floor of an atom-centric backward over
-the (N, C, D, D, D) layout.  Round 2: 40.8 / 56.5 / 67.2 / 79.6 MB per 50-grid
-step, against 83 MB of DRAM reads measured by ncu."""
+"""Index-backward footprint at 4-B, 32-B, 64-B and 128-B granularity: the
+DRAM-read floor of an atom-centric backward over the (N, C, D, D, D) layout.
+
+    python tools/footprint_granularity.py [c2|c5] [examples]
+
+Counts, over the first few examples of the bench batch (untransformed), the
+distinct grid_grad words / sectors / lines inside some same-channel atom's
+cutoff, scaled to a 50-grid step.  Round 2, C2: 40.8 / 56.5 / 67.2 / 79.6 MB
+against 83 MB of DRAM reads measured by ncu."""
 import sys
 
 sys.path.insert(0, "/root/repo")
@@ -9,14 +14,17 @@ import numpy as np
 
 import bench
 
-cfg = bench.CONFIGS["c2"]
+name = sys.argv[1] if len(sys.argv) > 1 else "c2"
+NEX = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+cfg = bench.CONFIGS[name]
 exs, _ = bench.make_batch(cfg, 0, 1)
-D, res, rmult = 48, 0.5, 1.5
-NEX = 6
+res = cfg["resolution"]
+D = int(round(cfg["dimension"] / res)) + 1
+rmult = 1.5
 counts = {4: 0, 32: 0, 64: 0, 128: 0}
 for ex in exs[:NEX]:
     sets = ex.coord_sets
-    origin = sets[-1].coords.astype(np.float64).mean(axis=0) - 11.75
+    origin = sets[-1].coords.astype(np.float64).mean(axis=0) - cfg["dimension"] / 2
     seen = {g: set() for g in counts}
     choff = 0
     for cs in sets:
@@ -40,5 +48,6 @@ for ex in exs[:NEX]:
         choff += cs.num_types
     for g in counts:
         counts[g] += len(seen[g])
+print(f"{name}: D={D}, {NEX} examples")
 for g, n in counts.items():
     print(f"{g:4d}-B granularity: {g * n / NEX * 50 / 1e6:7.1f} MB per 50-grid step")
