@@ -22,6 +22,7 @@ from __future__ import annotations
 import ctypes
 import math
 import os
+import threading
 
 import numpy as np
 import torch
@@ -238,6 +239,7 @@ class GridMaker:
         concatenated copies, ~1 ms for C2 vs ~9 ms to pack)."""
         sets = [cs for ss in example_sets for cs in ss]
         key = (tuple(id(cs) for cs in sets), tuple(len(ss) for ss in example_sets),
+               tuple(int(cs.num_types) for cs in sets),
                int(nchannels), str(device), float(self.radius_scale),
                bool(self.radius_type_indexed) and check_type_radii)
 
@@ -252,16 +254,29 @@ class GridMaker:
                     cat([np.asarray(cs.type_radii).reshape(-1) for cs in sets
                          if getattr(cs, "type_radii", None) is not None]))
 
-        cached = self.__dict__.get("_pack_cache")
+        # one entry per thread: a batch's workspace (its prepared records) is
+        # never shared by calls running concurrently on different threads
+        entries = self.__dict__.setdefault("_pack_cache", {})
+        tid = threading.get_ident()
+        cached = entries.get(tid)
         now = snap()
         if cached is not None and cached[0] == key and len(cached[2]) == len(now) and \
                 all(a.shape == b.shape and np.array_equal(a, b) for a, b in zip(cached[2], now)):
             return cached[1]
         pb = self.pack(example_sets, nchannels=nchannels, device=device,
                        check_type_radii=check_type_radii)
+        if len(entries) >= 8:  # threads come and go: keep the table small
+            entries.clear()
         # the set objects are kept alive with the entry, so their ids stay theirs
-        self.__dict__["_pack_cache"] = (key, pb, now, sets)
+        entries[tid] = (key, pb, now, sets)
         return pb
+
+    def __getstate__(self):
+        # estimator-style objects pickle / deepcopy as their parameters; the
+        # numpy API's pack cache (device buffers) stays behind
+        state = dict(self.__dict__)
+        state.pop("_pack_cache", None)
+        return state
 
     def _prepare(self, pb: PackedBatch, centers, transforms, npts) -> _native.GmParams:
         if centers is None:

@@ -224,6 +224,16 @@ def test_gridmaker_host_geometry_and_params():
         GridMaker().set_params(voxels=3)
     with pytest.raises(ValueError):
         GridMaker(radius_scale=-1.0).fit()
+    # estimator-style: pickles / deep-copies as its parameters, without the
+    # numpy API's per-thread pack cache (device buffers, unpicklable handles)
+    import copy
+    import pickle
+    import threading
+
+    gm = GridMaker(resolution=0.25, dimension=10.0)
+    gm.__dict__["_pack_cache"] = {threading.get_ident(): (None, threading.Lock())}
+    for clone in (pickle.loads(pickle.dumps(gm)), copy.deepcopy(gm)):
+        assert clone.get_params() == gm.get_params() and "_pack_cache" not in clone.__dict__
 
 
 @pytest.mark.parametrize("grm", [0.5, 1.0, 1.5, 2.0])

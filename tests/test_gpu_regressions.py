@@ -198,3 +198,41 @@ def test_numpy_api_pack_cache_hits_and_invalidates(monkeypatch):
     g2 = gm.forward_batch(exs)
     assert len(calls) == 2
     assert_close(g2, go.forward_batch(exs), what="repacked after an in-place change")
+
+
+def test_numpy_api_concurrent_threads_and_pickling():
+    """Threads sharing one GridMaker and the same examples each get their own
+    packed batch (the pack cache is per thread), so concurrent forward_batch
+    calls with different augmentation equal the sequential ones; a used
+    GridMaker still pickles / deep-copies as its parameters."""
+    import copy
+    import pickle
+    import threading
+
+    from paper_1912_04822_b200 import GridMaker, synthetic
+
+    exs = synthetic.batch(6, seed=3)
+    gm = GridMaker()
+    want = [gm.forward_batch(exs, random_rotation=True, random_translation=2.0,
+                             rng=np.random.default_rng(s)) for s in range(4)]
+    got = [None] * 4
+    barrier = threading.Barrier(4)
+
+    def work(s):
+        torch.cuda.set_device(0)
+        with torch.cuda.stream(torch.cuda.Stream()):
+            barrier.wait()
+            for _ in range(3):
+                got[s] = gm.forward_batch(exs, random_rotation=True, random_translation=2.0,
+                                          rng=np.random.default_rng(s))
+
+    ts = [threading.Thread(target=work, args=(s,)) for s in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for s in range(4):
+        np.testing.assert_array_equal(got[s], want[s])
+    for clone in (pickle.loads(pickle.dumps(gm)), copy.deepcopy(gm)):
+        assert clone.get_params() == gm.get_params()
+        np.testing.assert_array_equal(clone.forward_batch(exs[:2]), gm.forward_batch(exs[:2]))
