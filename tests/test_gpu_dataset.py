@@ -208,3 +208,35 @@ def test_vector_type_radii_required_when_type_indexed(vdata):
     exs, ds = vdata
     with pytest.raises(ConfigError, match="type_radii is missing"):
         ds.batch(4).assemble(GridMaker(radius_type_indexed=True), [0, 17, 18])
+
+
+def test_job_table_unstaged_group_counts():
+    """More (example, channel) groups than k_job_build stages in shared memory
+    (12032): 180 examples x 70 channels.  The device table still equals the
+    host builder's entry for entry, and the forward equals the host-packed one."""
+    from conftest import random_coordinate_set
+    from paper_1912_04822_b200 import Example, GridMaker, _native
+    from paper_1912_04822_b200.dataset import DeviceDataset
+
+    rng = np.random.default_rng(11)
+    exs = [Example(coord_sets=[random_coordinate_set(rng, int(rng.integers(0, 12)), 14, 6.0)
+                               for _ in range(5)]) for _ in range(180)]
+    ds = DeviceDataset(exs)
+    assert ds.nchannels == 70 and 180 * 70 > 12032
+    gm = GridMaker(resolution=1.0, dimension=12.0)
+    ids = rng.permutation(180)
+    ab = ds.batch(180).assemble(gm, ids)
+    pb = gm.pack([exs[i] for i in ids])
+    torch.cuda.synchronize()
+    N, C = pb.nexamples, pb.nchannels
+    p = gm._gm_params(gm.points_per_side())
+    co = np.ascontiguousarray(_host_array(pb, "chan_off", N * (C + 1)))
+    L = _native.lib()
+    cnt = L.gm_forward_jobs(ctypes.byref(p), N, C, co.ctypes.data, None, 0)
+    jobs = np.zeros((cnt, 4), np.int32)
+    L.gm_forward_jobs(ctypes.byref(p), N, C, co.ctypes.data, jobs.ctypes.data, cnt)
+    assert ab._gm.nfwd_jobs == cnt
+    np.testing.assert_array_equal(ab._jobs[:cnt].cpu().numpy(), jobs)
+    out, _ = gm.forward_packed(ab)
+    out2, _ = gm.forward_packed(pb)
+    assert torch.equal(out, out2)
