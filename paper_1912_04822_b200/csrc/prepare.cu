@@ -253,11 +253,22 @@ struct CallArgs {
 // index mode the position and the backward record (stored).
 // org: the call's origins (nex,3); xf: its transforms (nex,15) or null --
 // launch parameters (inline path) or the batch's device buffers.
-__device__ __forceinline__ void build_slot(const PrepArgs &A, const double *org,
-                                           const double *xf, int t, FwdItem &f, BinItem &bi) {
+// Index mode with slot records: loads and arithmetic only (nothing is
+// stored), so the pass can run this before its PDL wait -- while the previous
+// kernel on the workspace drains -- and store afterwards (store_slot).
+struct SlotOut {
+    FwdItem f;
+    BinItem bi;
+    BwdAtom w;
+    double x[3];
+    int a, bslot;
+};
+
+__device__ __forceinline__ void compute_slot(const PrepArgs &A, const double *org,
+                                             const double *xf, int t, SlotOut &o) {
     const gm_batch &b = A.b;
-    const bool vector = b.item_atom != nullptr;
-    if (!vector && b.slot_rec) {
+    FwdItem &f = o.f;
+    {
         const SlotRec R = reinterpret_cast<const SlotRec *>(b.slot_rec)[t];
         const gm_params &p = A.p;
         const int D = p.npts, e = R.ex, a = R.atom;
@@ -278,7 +289,11 @@ __device__ __forceinline__ void build_slot(const PrepArgs &A, const double *org,
                                                                             : p.matmul_order_n),
                                            X[9 + j]), X[12 + j]);
         }
-        store_pos(A, a, x);
+        o.x[0] = x[0];
+        o.x[1] = x[1];
+        o.x[2] = x[2];
+        o.a = a;
+        o.bslot = R.bslot;
         const double res = p.resolution, grm = p.gaussian_radius_multiple, rmult = p.radius_multiple;
         const double r = R.r;
         const double cut = p.binary ? r : __dmul_rn(r, rmult);
@@ -304,9 +319,9 @@ __device__ __forceinline__ void build_slot(const PrepArgs &A, const double *org,
         f.jbox = j0 | (j1 << 16);
         f.kbox = k0 | (k1 << 16);
         f.atom = a;
-        bi = BinItem{x[0], x[1], x[2], __dmul_rn(r, r)};
+        o.bi = BinItem{x[0], x[1], x[2], __dmul_rn(r, r)};
         // the backward's record (_kernels.py:224-251 constants, same box)
-        BwdAtom w;
+        BwdAtom &w = o.w;
         w.lx = x[0] - O[0];
         w.ly = x[1] - O[1];
         w.lz = x[2] - O[2];
@@ -323,8 +338,25 @@ __device__ __forceinline__ void build_slot(const PrepArgs &A, const double *org,
         w.ibox = f.ibox;
         w.jbox = f.jbox;
         w.kbox = f.kbox;
-        A.ws.batoms[R.bslot] = w;
-    } else {
+    }
+}
+
+__device__ __forceinline__ void store_slot(const PrepArgs &A, int t, const SlotOut &o) {
+    store_pos(A, o.a, o.x);
+    A.ws.batoms[o.bslot] = o.w;
+    A.ws.sorted[t] = o.f;
+    A.ws.sbox[t] = make_int2(o.f.ibox, o.f.jbox);
+    if (A.p.binary) A.ws.bsorted[t] = o.bi;
+}
+
+// Everything the prepare pass does for grouped slot t without slot records
+// (vector typing, or batches packed without them): loads, arithmetic and the
+// position / backward-record stores; the forward records are returned.
+__device__ __forceinline__ void build_slot(const PrepArgs &A, const double *org,
+                                           const double *xf, int t, FwdItem &f, BinItem &bi) {
+    const gm_batch &b = A.b;
+    const bool vector = b.item_atom != nullptr;
+    {
         const int it = b.item_perm[t];
         const int a = vector ? b.item_atom[it] : it;
         const int s = b.atom_set[a];
@@ -343,16 +375,23 @@ __device__ __forceinline__ void build_slot(const PrepArgs &A, const double *org,
 // they travel in K and the origins are copied out for forward / backward.
 template <int CAP, bool DEV>
 __global__ void __launch_bounds__(GM_PREP_THREADS) k_prepare_static(const PrepArgs A, const __grid_constant__ CallArgs<CAP> K) {
-    // PDL: the previous kernel (a backward reading this workspace) must be
-    // done before anything is written; then the forward may launch
-    pdl_wait();
-    pdl_trigger();
     const gm_batch &b = A.b;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int nex = b.nexamples;
     const bool vector = b.item_atom != nullptr;
     const double *org = DEV ? b.origins : K.v;
     const double *xf = DEV ? b.xforms : (K.has_xf ? K.v + 3 * nex : nullptr);
+    // Index mode with slot records: the slot's loads and arithmetic run before
+    // the PDL wait (they read only the batch's inputs, which no kernel of ours
+    // writes), overlapping the tail of the previous kernel on this workspace
+    const bool early = !vector && b.slot_rec && t < b.nitems;
+    SlotOut o;
+    if (early) compute_slot(A, org, xf, t, o);
+    // PDL: the previous kernel (a backward reading this workspace) must be
+    // done before anything is written; then the forward may launch
+    pdl_wait();
+    pdl_trigger();
+    if (early) store_slot(A, t, o);
     if (!DEV && t < 3 * nex) const_cast<double *>(b.origins)[t] = K.v[t];  // for forward / backward
     if (t < nex * (b.nchannels + 1)) A.ws.chan_off[t] = b.chan_off[t];
     if (vector && t < b.natoms) {  // positions of all atoms
@@ -365,7 +404,7 @@ __global__ void __launch_bounds__(GM_PREP_THREADS) k_prepare_static(const PrepAr
         if (b.bwd_slot) A.ws.atom_order[slot] = t;  // vector backward launch order
         store_vbwd_atom(A, t, s, e, org + 3 * e, x, slot);
     }
-    if (t < b.nitems) {
+    if (!early && t < b.nitems) {
         FwdItem f;
         BinItem bi;
         build_slot(A, org, xf, t, f, bi);
