@@ -347,13 +347,17 @@ def fresh_leg(args, cfg, gm, rank, ws, dev, stream, ev, barrier, out, tg, pool=1
 
     from paper_1912_04822_b200 import geom
     from paper_1912_04822_b200.dataset import DeviceDataset
+    from paper_1912_04822_b200.pipeline import DatasetBatches
 
     N = cfg["batch"]
     exs, _ = make_batch(cfg, rank, ws, n=max(pool, N))
     t0 = time.perf_counter()
     ds = DeviceDataset(exs, device=dev)
     build_s = time.perf_counter() - t0
-    ab = ds.batch(N)
+    frng = np.random.default_rng(4321)
+    # shuffled epochs; batch k + 1 assembled on a side stream during batch k
+    batches = DatasetBatches(gm, ds, N, shuffle=True, seed=4321, depth=2, prefetch=True)
+    ab = batches._ring[0]
     cap = ab.atom_capacity
     # vector typing: type gradients stay on the device (the CNN's side), sized
     # for the largest assembled batch
@@ -363,23 +367,11 @@ def fresh_leg(args, cfg, gm, rank, ws, dev, stream, ev, barrier, out, tg, pool=1
     host_cg = [torch.empty((cap, 3), dtype=torch.float32, pin_memory=True) for _ in range(2)]
     copy_s = torch.cuda.Stream(device=dev)
     done = [torch.cuda.Event(), torch.cuda.Event()]
-    frng = np.random.default_rng(4321)
-    order = frng.permutation(len(exs))
-    pos = [0]
     nbytes = [0, 0]
-
-    def next_ids():
-        nonlocal order
-        if pos[0] + N > len(order):
-            order = frng.permutation(len(exs))
-            pos[0] = 0
-        ids = order[pos[0]:pos[0] + N]
-        pos[0] += N
-        return ids
 
     def step(k):
         x = k % 2
-        ab.assemble(gm, next_ids())
+        ab = next(batches)
         xf = geom.draw_transform_array(ab.default_centers, 2.0, True, frng)
         o = out[:ab.nexamples]
         gm.forward_packed(ab, o, transforms=xf)
@@ -426,7 +418,9 @@ def fresh_leg(args, cfg, gm, rank, ws, dev, stream, ev, barrier, out, tg, pool=1
             "note": "fresh shuffled batches every step from a device-resident pool "
                     "(DeviceDataset, uploaded once): gm_assemble builds each batch and its "
                     "job table on the device, then prepare/forward/backward of loss "
-                    "1/2|grid|^2 and a D2H of the coordinate gradients; per-step H2D = the "
+                    "1/2|grid|^2 and a D2H of the coordinate gradients (batch k + 1 is assembled on a "
+                    "high-priority side stream while batch k grids: DatasetBatches(prefetch=True)); "
+                    "per-step H2D = the "
                     "index list + transforms (kernel-launch parameters)"}
 
 

@@ -122,14 +122,21 @@ class DatasetBatches:
     packing runs on the GPU (``gm_assemble``), stream-ordered, with nothing
     left on the host to overlap.  ``shuffle`` draws a new permutation of the
     dataset every epoch (``seed``); batches never straddle epochs -- the
-    last one of an epoch may be smaller unless ``drop_last``.  ``depth``
-    batch objects are recycled in a ring, so the ``depth - 1`` previous
-    batches stay valid while the next one is assembled.  Each yielded batch
-    carries ``ids`` (its dataset indices, in order).
+    last one of an epoch may be smaller unless ``drop_last``.  Batch objects
+    are recycled in a ring, so the ``depth - 1`` previous batches stay valid
+    while the next one is assembled.  Each yielded batch carries ``ids`` (its
+    dataset indices, in order).
+
+    ``prefetch``: batch k + 1 is assembled on a high-priority side stream
+    while the consumer's stream runs batch k's work (its assembly kernels
+    fill SM slots the gridding leaves free), and the consumer's current
+    stream waits for it when it is yielded.  The consumer must enqueue its
+    work on a batch on the stream that is current when it calls ``next``.
     """
 
     def __init__(self, gm, dataset, batch_size: int, shuffle: bool = True, seed=None,
-                 depth: int = 2, drop_last: bool = False, max_batches=None):
+                 depth: int = 2, drop_last: bool = False, max_batches=None,
+                 prefetch: bool = False):
         self.gm = gm
         self.dataset = dataset
         self.batch_size = int(batch_size)
@@ -139,7 +146,13 @@ class DatasetBatches:
         self.rng = np.random.default_rng(seed)
         self.drop_last = bool(drop_last)
         self.max_batches = max_batches
-        self._ring = [dataset.batch(self.batch_size) for _ in range(max(1, int(depth)))]
+        self.prefetch = bool(prefetch)
+        # one more ring slot with prefetch: the batch being assembled ahead
+        nring = max(1, int(depth)) + (1 if self.prefetch else 0)
+        self._ring = [dataset.batch(self.batch_size) for _ in range(nring)]
+        self._side = (torch.cuda.Stream(device=dataset.device, priority=-1)
+                      if self.prefetch else None)
+        self._pending = None  # (batch, ready event) assembled ahead
         self._k = 0
         self._order = None
         self._pos = 0
@@ -160,6 +173,23 @@ class DatasetBatches:
     def __next__(self):
         if self.max_batches is not None and self._k >= self.max_batches:
             raise StopIteration
-        ab = self._ring[self._k % len(self._ring)]
+        cur = torch.cuda.current_stream(self.dataset.device)
+        if self._pending is None:
+            ab = self._ring[self._k % len(self._ring)].assemble(self.gm, self._next_ids())
+        else:
+            ab, ready = self._pending
+            cur.wait_event(ready)
+            self._pending = None
         self._k += 1
-        return ab.assemble(self.gm, self._next_ids())
+        if self.prefetch and (self.max_batches is None or self._k < self.max_batches):
+            # the slot of batch k + 1 - len(ring): its work is already on `cur`
+            nxt = self._ring[self._k % len(self._ring)]
+            free = torch.cuda.Event()
+            free.record(cur)
+            ready = torch.cuda.Event()
+            with torch.cuda.stream(self._side):
+                self._side.wait_event(free)
+                nxt.assemble(self.gm, self._next_ids())
+                ready.record(self._side)
+            self._pending = (nxt, ready)
+        return ab

@@ -99,3 +99,36 @@ def test_dataset_batches_epochs_and_parity():
     assert sorted(sum(seen[:3], [])) == list(range(10))
     assert sorted(sum(seen[3:], [])) == list(range(10))
     assert seen[:3] != seen[3:]  # a new permutation each epoch
+
+
+def test_dataset_batches_prefetch_matches_serial():
+    """DatasetBatches(prefetch=True) assembles batch k + 1 on a side stream
+    while the consumer grids batch k: same index lists, and grids / gradients
+    bit-identical to the serial iterator, the previous batch still intact."""
+    from paper_1912_04822_b200 import GridMaker, geom, synthetic
+    from paper_1912_04822_b200.dataset import DeviceDataset
+    from paper_1912_04822_b200.pipeline import DatasetBatches
+
+    rng = np.random.default_rng(8)
+    exs = [synthetic.complex_example(rng, n_receptor=300) for _ in range(23)]
+    gm = GridMaker()
+    ds = DeviceDataset(exs)
+    runs = []
+    for prefetch in (False, True):
+        it = DatasetBatches(gm, ds, batch_size=5, seed=9, depth=2, prefetch=prefetch,
+                            max_batches=9)
+        got, prev = [], None
+        for k, ab in enumerate(it):
+            xf = geom.draw_transform_array(ab.default_centers, 2.0, True, np.random.default_rng(k))
+            grid, _ = gm.forward_packed(ab, transforms=xf)
+            cg, _ = gm.backward_packed(ab, grid, reuse_prepared=True)
+            if prev is not None:  # depth 2: the previous batch is still valid
+                pab, pids = prev
+                assert list(pab.ids) == pids
+            prev = (ab, list(ab.ids))
+            got.append((list(ab.ids), grid.cpu(), cg.cpu()))
+        assert len(got) == 9
+        runs.append(got)
+    for (i0, g0, c0), (i1, g1, c1) in zip(*runs):
+        assert i0 == i1
+        assert torch.equal(g0, g1) and torch.equal(c0, c1)
