@@ -75,14 +75,15 @@ while True:
               pynvml.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)
     except Exception:
         break
-    time.sleep(0.0005)
+    time.sleep(float(sys.argv[2]))
 """
 
 
 class ClockSampler:
     """SM clocks and throttle reasons sampled by NVML during the timed region,
     in a separate process (a sampling thread would steal the GIL from the
-    launch loop and open gaps on the device)."""
+    launch loop and open gaps on the device).  Every GM_CLOCK_INTERVAL
+    seconds (default 0.5 ms; 0.5 / 2 / 5 / 20 ms gave the same C2 step)."""
 
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
@@ -101,7 +102,8 @@ class ClockSampler:
                 idx = self.index
         self.nvml_index = idx
         try:
-            self.proc = subprocess.Popen([sys.executable, "-c", _CLOCK_PROBE, str(idx)],
+            self.proc = subprocess.Popen([sys.executable, "-c", _CLOCK_PROBE, str(idx),
+                                          os.environ.get("GM_CLOCK_INTERVAL", "0.0005")],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                                          text=True)
             first = self.proc.stdout.readline().split()  # wait until NVML is up

@@ -33,3 +33,16 @@ e1.record()
 torch.cuda.synchronize()
 t2 = time.perf_counter()
 print("host issue per step", (t1 - t0) / 50 * 1e6, "us; device per step", e0.elapsed_time(e1) / 50 * 1e3, "us; wall", (t2 - t0) / 50 * 1e6)
+# the same loop with one fixed transform array (no per-step draw)
+xf = geom.draw_transform_array(centers, 2.0, True, rng)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+e0.record()
+for _ in range(50):
+    gm.forward_packed(pb, out, transforms=xf)
+    gm.backward_packed(pb, gg, reuse_prepared=True, coord_grad=cg)
+t1 = time.perf_counter()
+e1.record()
+torch.cuda.synchronize()
+print("fixed xf: host issue per step", (t1 - t0) / 50 * 1e6, "us; device per step",
+      e0.elapsed_time(e1) / 50 * 1e3, "us")
