@@ -1,0 +1,92 @@
+"""Randomised parity sweep: many small random configurations (resolution,
+dimension, radius scale, Gaussian radius multiple, binary, index / vector
+typing, type-indexed radii, empty and single-atom sets, atoms outside the
+grid, augmentation on / off), each compared with the CPU oracle -- binary
+bit-exact, smooth grids and gradients within the north star's tolerance."""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from parity import assert_close
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _random_case(seed):
+    from paper_1912_04822_b200 import Example
+    from paper_1912_04822_b200.coordsets import CoordinateSet
+
+    rng = np.random.default_rng(1000 + seed)
+    res = float(rng.choice([0.2, 0.25, 0.3, 0.375, 0.5, 0.7, 1.0, 1.6]))
+    dim = float(np.round(rng.uniform(0.0, 16.0) / res) * res * rng.choice([1.0, 1.0, 1.03]))
+    cfg = dict(resolution=res, dimension=dim, binary=bool(rng.random() < 0.25),
+               radius_scale=float(rng.choice([1.0, 1.0, 0.7, 1.3])),
+               gaussian_radius_multiple=float(rng.choice([1.0, 1.0, 0.6, 1.5])))
+    vector = bool(rng.random() < 0.35)
+    cfg["radius_type_indexed"] = bool(vector and rng.random() < 0.5)
+    nex = int(rng.integers(1, 6))
+    nsets = int(rng.integers(1, 4))
+    T = [int(rng.integers(1, 9)) for _ in range(nsets)]
+    exs = []
+    for _ in range(nex):
+        sets = []
+        for s in range(nsets):
+            n = int(rng.choice([0, 1, 2, 5, 17, 40]))
+            spread = dim / 2 + 3.0
+            coords = rng.uniform(-spread, spread, (n, 3)).astype(np.float32)
+            if n and rng.random() < 0.3:  # some atoms exactly on voxel centres / duplicated
+                k = int(rng.integers(1, n + 1))
+                coords[:k] = (np.round(coords[:k] / res) * res).astype(np.float32)
+                coords[k // 2] = coords[0]
+            radii = rng.uniform(0.6, 3.0 if rng.random() < 0.2 else 2.2, n).astype(np.float32)
+            if vector:
+                tv = (rng.random((n, T[s])) * (rng.random((n, T[s])) < 0.4)).astype(np.float32)
+                cs = CoordinateSet(coords=coords, radii=radii, num_types=T[s], type_vector=tv,
+                                   type_radii=rng.uniform(0.8, 2.0, T[s]).astype(np.float32))
+            else:
+                cs = CoordinateSet(coords=coords, radii=radii, num_types=T[s],
+                                   type_index=rng.integers(0, T[s], n))
+            sets.append(cs)
+        exs.append(Example(coord_sets=sets))
+    aug = dict(random_rotation=bool(rng.random() < 0.6),
+               random_translation=float(rng.choice([0.0, 0.0, 1.0, 2.5])))
+    return cfg, exs, aug
+
+
+# GM_FUZZ_CASES widens the sweep (exploratory runs); the suite runs 40 cases
+@pytest.mark.parametrize("seed", range(int(os.environ.get("GM_FUZZ_CASES", "40"))))
+def test_random_configuration_vs_oracle(seed):
+    from paper_1912_04822_b200 import GridMaker
+
+    cfg, exs, aug = _random_case(seed)
+    gm = GridMaker(**cfg)
+    go = oracle.GridOracle(**cfg)
+    got, xf = gm.forward_batch(exs, rng=np.random.default_rng(seed), return_transforms=True,
+                               **aug)
+    ref = go.forward_batch(exs, rng=np.random.default_rng(seed), **aug)
+    assert got.shape == ref.shape
+    if cfg["binary"]:
+        np.testing.assert_array_equal(got, ref, err_msg=f"case {seed}: {cfg}")
+        return
+    assert_close(got, ref, what=f"case {seed} forward {cfg}")
+    gg = np.random.default_rng(seed + 7).standard_normal(ref.shape).astype(np.float32)
+    res = gm.backward_batch(exs, gg, transforms=xf)
+    cgs, tgs = go.backward_batch(exs, gg, rng=np.random.default_rng(seed), **aug)
+    got_cg = np.concatenate([c for ex in res for (c, _) in ex]) if res else np.zeros((0, 3))
+    assert_close(got_cg, np.concatenate(cgs) if cgs else np.zeros((0, 3)),
+                 what=f"case {seed} coordinate gradients {cfg}")
+    got_tg = [t for ex in res for (_, t) in ex]
+    if any(t is not None for t in got_tg):
+        assert_close(np.concatenate([t.reshape(-1) for t in got_tg]),
+                     np.concatenate([np.asarray(t).reshape(-1) for t in tgs]),
+                     what=f"case {seed} type gradients {cfg}")
