@@ -90,3 +90,32 @@ def test_random_configuration_vs_oracle(seed):
         assert_close(np.concatenate([t.reshape(-1) for t in got_tg]),
                      np.concatenate([np.asarray(t).reshape(-1) for t in tgs]),
                      what=f"case {seed} type gradients {cfg}")
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("GM_FUZZ_CASES", "40"))))
+def test_random_configuration_assembled_equals_packed(seed):
+    """The same random cases through a DeviceDataset: the device-assembled
+    batch grids and back-propagates bit for bit like the host-packed one."""
+    from paper_1912_04822_b200 import GridMaker, geom
+    from paper_1912_04822_b200.dataset import DeviceDataset
+
+    cfg, exs, aug = _random_case(seed)
+    gm = GridMaker(**cfg)
+    ds = DeviceDataset(exs)
+    ab = ds.batch(len(exs)).assemble(gm, np.arange(len(exs))[::-1].copy())
+    pb = gm.pack(exs[::-1])
+    xf = geom.draw_transform_array(ab.default_centers, aug["random_translation"],
+                                   aug["random_rotation"], np.random.default_rng(seed))
+    if ab.natoms == 0:
+        return
+    out, _ = gm.forward_packed(ab, transforms=xf)
+    out2, _ = gm.forward_packed(pb, transforms=xf)
+    assert torch.equal(out, out2), f"case {seed}: assembled grids differ {cfg}"
+    if cfg["binary"]:
+        return
+    gg = torch.randn_like(out)
+    cg, tg = gm.backward_packed(ab, gg, reuse_prepared=True)
+    cg2, tg2 = gm.backward_packed(pb, gg, reuse_prepared=True)
+    assert torch.equal(cg, cg2), f"case {seed}: assembled coordinate gradients differ {cfg}"
+    if tg is not None:
+        assert torch.equal(tg, tg2), f"case {seed}: assembled type gradients differ {cfg}"
