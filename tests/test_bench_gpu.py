@@ -34,3 +34,16 @@ def test_bench_json_line_contract():
     assert r["fwd_cutoff_pairs_per_s"] > 0 and r["bwd_cutoff_pairs_per_s"] > 0
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+
+
+@pytest.mark.gpu
+def test_bench_latency_config_graph_leg():
+    """C1 (one ligand per call): the line carries the CUDA-graph replay rate
+    beside the eager headline, and the replay is the faster of the two."""
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--config", "c1", "--steps", "20",
+                          "--warmup", "3", "--no-cpu-baseline"],
+                         capture_output=True, text=True, timeout=600, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    g = d["graph"]
+    assert g["unit"] == "grids/s" and g["value"] > d["value"] > 0
