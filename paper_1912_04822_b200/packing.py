@@ -15,6 +15,7 @@ per-call arrays (origins, transforms) are uploaded separately.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 
@@ -501,8 +502,34 @@ def _default_center(sets) -> np.ndarray:
     return np.zeros(3, dtype=np.float64)
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+_get_device = getattr(torch._C, "_cuda_getDevice", None)
+
+
+def device_index(device) -> int:
+    if isinstance(device, torch.device) and device.index is not None:
+        return device.index
+    if isinstance(device, int):
+        return device
+    return torch.cuda.current_device() if device is None or torch.device(device).index is None \
+        else torch.device(device).index
+
+
 def stream_handle(device) -> int:
+    """cudaStream_t of torch's current stream on ``device`` (the stream every
+    call is ordered on).  The raw query skips the Stream object torch would
+    build (a few us per call: small batches are bound by host launch work)."""
+    if _raw_stream is not None:
+        return _raw_stream(device_index(device))
     return torch.cuda.current_stream(device).cuda_stream
+
+
+def on_device(device):
+    """``torch.cuda.device(device)``, or nothing when it is already current."""
+    idx = device_index(device)
+    if _get_device is not None and _get_device() == idx:
+        return contextlib.nullcontext()
+    return torch.cuda.device(idx)
 
 
 def as_ptr(t: torch.Tensor | None):

@@ -30,7 +30,7 @@ import torch
 from . import _native, export, geom, hostio
 from .coordsets import coord_sets_of, is_coordinate_set
 from .errors import DeviceError
-from .packing import PackedBatch, stream_handle
+from .packing import PackedBatch, on_device, stream_handle
 from .validation import check_rng, check_vector3
 
 
@@ -312,7 +312,7 @@ class GridMaker:
             b = pb.gm_batch()
             org = np.ascontiguousarray(origins, np.float64)
             xf = None if xforms is None else np.ascontiguousarray(xforms, np.float64)
-            with torch.cuda.device(pb.device):
+            with on_device(pb.device):
                 _native.check(_native.lib().gm_prepare_inline(
                     ctypes.byref(p), ctypes.byref(b), pb.workspace.data_ptr(),
                     pb.workspace_bytes, org.ctypes.data, None if xf is None else xf.ctypes.data,
@@ -320,7 +320,7 @@ class GridMaker:
             return p
         pb.set_call_arrays(origins, xforms)
         b = pb.gm_batch()
-        with torch.cuda.device(pb.device):
+        with on_device(pb.device):
             _native.check(_native.lib().gm_prepare(
                 ctypes.byref(p), ctypes.byref(b), pb.workspace.data_ptr(), pb.workspace_bytes,
                 stream_handle(pb.device)))
@@ -350,7 +350,7 @@ class GridMaker:
                                                        bool(random_rotation), rng)
         p = self._prepare(pb, centers, transforms, npts)
         if pb.nexamples and pb.nchannels:
-            with torch.cuda.device(pb.device):
+            with on_device(pb.device):
                 pb.ensure_fwd_jobs(p)
                 if events is not None:
                     events[0].record()
@@ -393,7 +393,7 @@ class GridMaker:
             coord_grad = torch.empty((pb.natoms, 3), dtype=torch.float32, device=pb.device)
         if pb.vector_mode and type_grad is None:
             type_grad = torch.empty((pb.nweights,), dtype=torch.float32, device=pb.device)
-        with torch.cuda.device(pb.device):
+        with on_device(pb.device):
             if events is not None:
                 events[0].record()
             _native.check(_native.lib().gm_backward(
