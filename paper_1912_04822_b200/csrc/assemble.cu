@@ -12,6 +12,8 @@
 // order), writes its set rows, channel offsets and nonzero-channel list.  The
 // forward job table follows on the device (forward.cu: k_job_build).  Batch
 // sizes come from the dataset's host mirrors: no sync.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace {
@@ -34,19 +36,23 @@ struct __align__(16) SlotOut {
 };
 static_assert(sizeof(SlotOut) == 48, "SlotOut must be 48 bytes");
 
+// CAP: examples the launch parameters hold (8, 64 or GM_INLINE_MAX_EXAMPLES):
+// the smallest that fits, so small batches launch with small parameter blocks
+template <int CAP>
 struct AsmArgs {
     gm_dataset ds;
     gm_batch b;
     double scale;
     int n;
-    int4 ex[GM_INLINE_MAX_EXAMPLES];  // per batch example: id, atom base, set base, seg base
+    int4 ex[CAP];  // per batch example: id, atom base, set base, seg base
 };
 
 // grid (batch example, atom chunk of kAsmChunk): chunk 0 also writes the
 // example's set rows, channel offsets and nonzero-channel list
 constexpr int kAsmChunk = 256;
 
-__global__ void __launch_bounds__(256) k_assemble(const __grid_constant__ AsmArgs A) {
+template <int CAP>
+__global__ void __launch_bounds__(256) k_assemble(const __grid_constant__ AsmArgs<CAP> A) {
     const int bi = blockIdx.x, tid = threadIdx.x;
     const int q0 = blockIdx.y * kAsmChunk;
     const int4 X = A.ex[bi];
@@ -131,17 +137,19 @@ struct __align__(16) DsItem {
 };
 static_assert(sizeof(DsItem) == 16, "DsItem must be 16 bytes");
 
+template <int CAP>
 struct VAsmArgs {
     gm_dataset ds;
     gm_batch b;
     double scale;
     int rti;
     int n;
-    int4 ex[GM_INLINE_MAX_EXAMPLES];   // id, atom base, set base, seg base
-    int4 ex2[GM_INLINE_MAX_EXAMPLES];  // item base, weight base, type-radius base, -
+    int4 ex[CAP];   // id, atom base, set base, seg base
+    int4 ex2[CAP];  // item base, weight base, type-radius base, -
 };
 
-__global__ void __launch_bounds__(256) k_assemble_vector(const __grid_constant__ VAsmArgs A) {
+template <int CAP>
+__global__ void __launch_bounds__(256) k_assemble_vector(const __grid_constant__ VAsmArgs<CAP> A) {
     const int bi = blockIdx.x, tid = threadIdx.x, y = blockIdx.y;
     const int4 X = A.ex[bi], X2 = A.ex2[bi];
     const int id = X.x, abase = X.y, sbase = X.z, gbase = X.w;
@@ -285,28 +293,35 @@ gm_status assemble_impl(const gm_params *p, const gm_dataset *ds, const int32_t 
     b->fwd_jobs = jobs;
     b->nfwd_jobs = (int32_t)njobs;
     b->fwd_jobs_npts = p->npts;
-    if (vec) {
-        VAsmArgs V;
-        V.ds = *ds;
-        V.b = *b;
-        V.scale = p->radius_scale;
-        V.rti = p->radius_type_indexed ? 1 : 0;
-        V.n = n;
-        memcpy(V.ex, ex, sizeof(int4) * n);
-        memcpy(V.ex2, ex2, sizeof(int4) * n);
-        const int ch = std::max(std::max((maxa + kAsmChunk - 1) / kAsmChunk,
-                                         (maxi + kAsmChunk - 1) / kAsmChunk),
-                                std::max(1, (maxw + 16 * kAsmChunk - 1) / (16 * kAsmChunk)));
-        k_assemble_vector<<<dim3(n, (unsigned)std::max(1, ch)), 256, 0, s>>>(V);
-    } else {
-        AsmArgs A;
-        A.ds = *ds;
-        A.scale = p->radius_scale;
-        A.n = n;
-        memcpy(A.ex, ex, sizeof(int4) * n);
-        A.b = *b;
-        k_assemble<<<dim3(n, (unsigned)std::max(1, (maxa + kAsmChunk - 1) / kAsmChunk)), 256, 0, s>>>(A);
-    }
+    const int chunks_idx = std::max(1, (maxa + kAsmChunk - 1) / kAsmChunk);
+    const int chunks_vec = std::max(std::max((maxa + kAsmChunk - 1) / kAsmChunk,
+                                             (maxi + kAsmChunk - 1) / kAsmChunk),
+                                    std::max(1, (maxw + 16 * kAsmChunk - 1) / (16 * kAsmChunk)));
+    auto launch = [&](auto capc) {
+        constexpr int CAP = decltype(capc)::value;
+        if (vec) {
+            VAsmArgs<CAP> V;
+            V.ds = *ds;
+            V.b = *b;
+            V.scale = p->radius_scale;
+            V.rti = p->radius_type_indexed ? 1 : 0;
+            V.n = n;
+            memcpy(V.ex, ex, sizeof(int4) * n);
+            memcpy(V.ex2, ex2, sizeof(int4) * n);
+            k_assemble_vector<CAP><<<dim3(n, (unsigned)std::max(1, chunks_vec)), 256, 0, s>>>(V);
+        } else {
+            AsmArgs<CAP> A;
+            A.ds = *ds;
+            A.scale = p->radius_scale;
+            A.n = n;
+            memcpy(A.ex, ex, sizeof(int4) * n);
+            A.b = *b;
+            k_assemble<CAP><<<dim3(n, (unsigned)chunks_idx), 256, 0, s>>>(A);
+        }
+    };
+    if (n <= 8) launch(std::integral_constant<int, 8>{});
+    else if (n <= 64) launch(std::integral_constant<int, 64>{});
+    else launch(std::integral_constant<int, GM_INLINE_MAX_EXAMPLES>{});
     LAUNCH_CHECK();
     return forward_jobs_device(p, n, C, b->chan_off, jobs, nsegs, G - nsegs,
                                reinterpret_cast<int4 *>(jobs + 4 * njobs), s);

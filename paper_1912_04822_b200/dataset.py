@@ -25,7 +25,7 @@ import torch
 
 from . import _native, errors
 from .coordsets import coord_sets_of
-from .packing import PackedBatch, _default_center, _Layout, stream_handle
+from .packing import PackedBatch, _default_center, _Layout, on_device, stream_handle
 
 # gm_dataset.records entry (include/gridmaker_b200.h)
 _DS_DTYPE = np.dtype([("x", "<f4"), ("y", "<f4"), ("z", "<f4"), ("r", "<f4"), ("atom", "<i4"),
@@ -360,9 +360,10 @@ class AssembledBatch(PackedBatch):
         return np.repeat(np.arange(len(self.ids), dtype=np.int32), counts)
 
     # -- assembly ----------------------------------------------------------------
-    def assemble(self, gm, ids) -> "AssembledBatch":
+    def assemble(self, gm, ids, stream=None) -> "AssembledBatch":
         """Make this batch the examples ``ids`` of the dataset (in that order),
-        for ``gm``'s grid; stream-ordered on the current stream, no host sync."""
+        for ``gm``'s grid; stream-ordered on ``stream`` (default: the current
+        stream), no host sync."""
         ids = np.ascontiguousarray(ids, dtype=np.int32).reshape(-1)
         if not 1 <= ids.shape[0] <= self.capacity:
             raise ValueError(f"batch of {ids.shape[0]} examples, capacity {self.capacity}")
@@ -375,7 +376,7 @@ class AssembledBatch(PackedBatch):
         self.default_centers = self.dataset.centers[ids]
         self._origin_key = None  # GridMaker._prepare caches origins per batch
         self._last_params = None
-        self._assemble(gm._gm_params(gm.points_per_side()))
+        self._assemble(gm._gm_params(gm.points_per_side()), stream)
         return self
 
     def _job_capacity(self, params) -> int:
@@ -388,7 +389,7 @@ class AssembledBatch(PackedBatch):
         cnt = _native.lib().gm_forward_jobs(ctypes.byref(params), n, C, full.ctypes.data, None, 0)
         return int(cnt) + 2 * n * C
 
-    def _assemble(self, params) -> None:
+    def _assemble(self, params, stream=None) -> None:
         if self._jobs_cap == 0 or getattr(self, "_jobs_cap_npts", None) != int(params.npts):
             need = self._job_capacity(params)
             if need > self._jobs_cap:
@@ -396,11 +397,12 @@ class AssembledBatch(PackedBatch):
                 self._jobs_cap = need
             self._jobs_cap_npts = int(params.npts)
         self._cap.jobs = self._jobs_cap
-        with torch.cuda.device(self.device):
+        sh = stream.cuda_stream if stream is not None else stream_handle(self.device)
+        with on_device(self.device):
             _native.check(_native.lib().gm_assemble(
                 ctypes.byref(params), ctypes.byref(self.dataset._ds), self.ids.ctypes.data,
                 int(self.ids.shape[0]), ctypes.byref(self._gm), ctypes.byref(self._cap),
-                self._jobs.data_ptr(), stream_handle(self.device)))
+                self._jobs.data_ptr(), sh))
         g = self._gm
         self.nexamples, self.natoms, self.nitems, self.nsets = \
             g.nexamples, g.natoms, g.nitems, g.nsets

@@ -152,6 +152,9 @@ class DatasetBatches:
         self._ring = [dataset.batch(self.batch_size) for _ in range(nring)]
         self._side = (torch.cuda.Stream(device=dataset.device, priority=-1)
                       if self.prefetch else None)
+        # per ring slot: "the consumer's work on it is enqueued" / "assembled"
+        self._free = [torch.cuda.Event() for _ in self._ring] if self.prefetch else None
+        self._ready = [torch.cuda.Event() for _ in self._ring] if self.prefetch else None
         self._pending = None  # (batch, ready event) assembled ahead
         self._k = 0
         self._order = None
@@ -173,23 +176,21 @@ class DatasetBatches:
     def __next__(self):
         if self.max_batches is not None and self._k >= self.max_batches:
             raise StopIteration
-        cur = torch.cuda.current_stream(self.dataset.device)
         if self._pending is None:
             ab = self._ring[self._k % len(self._ring)].assemble(self.gm, self._next_ids())
         else:
             ab, ready = self._pending
-            cur.wait_event(ready)
+            torch.cuda.current_stream(self.dataset.device).wait_event(ready)
             self._pending = None
         self._k += 1
         if self.prefetch and (self.max_batches is None or self._k < self.max_batches):
-            # the slot of batch k + 1 - len(ring): its work is already on `cur`
-            nxt = self._ring[self._k % len(self._ring)]
-            free = torch.cuda.Event()
-            free.record(cur)
-            ready = torch.cuda.Event()
-            with torch.cuda.stream(self._side):
-                self._side.wait_event(free)
-                nxt.assemble(self.gm, self._next_ids())
-                ready.record(self._side)
+            # the slot of batch k + 1 - len(ring): its work is already on the
+            # current stream, which the side stream waits for
+            slot = self._k % len(self._ring)
+            nxt, free, ready = self._ring[slot], self._free[slot], self._ready[slot]
+            free.record()
+            self._side.wait_event(free)
+            nxt.assemble(self.gm, self._next_ids(), stream=self._side)
+            ready.record(self._side)
             self._pending = (nxt, ready)
         return ab
