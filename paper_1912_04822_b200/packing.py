@@ -507,12 +507,13 @@ _get_device = getattr(torch._C, "_cuda_getDevice", None)
 
 
 def device_index(device) -> int:
-    if isinstance(device, torch.device) and device.index is not None:
-        return device.index
+    """CUDA device ordinal of ``device`` (torch.device, 'cuda:N', int; the
+    current device when it names none)."""
     if isinstance(device, int):
         return device
-    return torch.cuda.current_device() if device is None or torch.device(device).index is None \
-        else torch.device(device).index
+    if not isinstance(device, torch.device):
+        device = torch.device("cuda" if device is None else device)
+    return device.index if device.index is not None else torch.cuda.current_device()
 
 
 def stream_handle(device) -> int:
