@@ -272,6 +272,22 @@ gm_status gm_backward_vector_host(double *coord_grad, double *type_grad, const d
                                   const double *type_radii, int32_t radius_type_indexed,
                                   const double *origin, double res, double grm, double rmult);
 
+/* ---- MOLC cache records -> typed atoms ----
+ *
+ * Replaces the reference's per-atom decode and typing of a cache entry
+ * (chemio.py:353-356 RawAtom objects, atomtypes.py:272-291 type_molecule with
+ * the default element typer).  raw: device, the 13-byte records (u8 element,
+ * f32 x, y, z little-endian) of nentries entries back to back; entry_start:
+ * device (nentries+1) int64 atom offsets of the entries in raw; type_table:
+ * device (256) int16, element number -> type index or -1 (atom dropped);
+ * type_radii: device, radius per type.  Writes, in record order with dropped
+ * atoms removed: coords (kept,3) f32, type_index (kept) int32, radius (kept)
+ * f32, and offsets (nentries+1) int64 (entry e owns [offsets[e],
+ * offsets[e+1])).  Output arrays must hold entry_start[nentries] atoms. */
+gm_status gm_molc_decode(const uint8_t *raw, const int64_t *entry_start, int32_t nentries,
+                         const int16_t *type_table, const float *type_radii, float *coords,
+                         int32_t *type_index, float *radius, int64_t *offsets, void *stream);
+
 /* ---- host helpers ---- */
 
 /* geom.make_transform for n examples from pre-drawn uniforms (geom.py:66-76,

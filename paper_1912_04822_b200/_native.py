@@ -97,6 +97,7 @@ EXPORTS = (
     "gm_backward_vector_host", "gm_last_error", "gm_version", "gm_device_count",
     "gm_launch_count", "gm_struct_size", "gm_draw_transforms", "gm_forward_jobs",
     "gm_assemble",
+    "gm_molc_decode",
 )
 
 
@@ -146,6 +147,8 @@ def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     L.gm_assemble.argtypes = [P(GmParams), P(GmDataset), _vp, _c_int32, P(GmBatch),
                               P(GmCapacity), _vp, _vp]
     L.gm_assemble.restype = ctypes.c_int
+    L.gm_molc_decode.argtypes = [_vp, _vp, _c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+    L.gm_molc_decode.restype = ctypes.c_int
     L.gm_draw_transforms.argtypes = [_vp, _c_int64, _c_int32, _c_double, _vp, _vp]
     L.gm_draw_transforms.restype = ctypes.c_int
     L.gm_last_error.restype = ctypes.c_char_p

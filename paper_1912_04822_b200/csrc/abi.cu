@@ -227,6 +227,22 @@ extern "C" gm_status gm_assemble(const gm_params *p, const gm_dataset *ds, const
     return assemble_impl(p, ds, ids, n, b, cap, jobs, (cudaStream_t)stream);
 }
 
+gm_status molc_decode_impl(const uint8_t *raw, const int64_t *entry_start, int32_t nentries,
+                           const int16_t *type_table, const float *type_radii, float *coords,
+                           int32_t *type_index, float *radius, int64_t *offsets, cudaStream_t s);
+
+extern "C" gm_status gm_molc_decode(const uint8_t *raw, const int64_t *entry_start, int32_t nentries,
+                                    const int16_t *type_table, const float *type_radii,
+                                    float *coords, int32_t *type_index, float *radius,
+                                    int64_t *offsets, void *stream) {
+    if (nentries < 0) return gm_fail(GM_ERR_INVALID, "nentries %d < 0", nentries);
+    if (!offsets || (nentries > 0 && (!raw || !entry_start || !type_table || !type_radii ||
+                                      !coords || !type_index || !radius)))
+        return gm_fail(GM_ERR_INVALID, "NULL argument");
+    return molc_decode_impl(raw, entry_start, nentries, type_table, type_radii, coords, type_index,
+                            radius, offsets, (cudaStream_t)stream);
+}
+
 extern "C" gm_status gm_backward(const gm_params *p, const gm_batch *b, const void *workspace,
                                  const float *grid_grad, float *coord_grad, float *type_grad,
                                  void *stream) {

@@ -11,8 +11,9 @@ its 13-byte records; typing is a table lookup over the element column.
   bit for bit (same f32 coordinates, atom order, radii, types).
 * ``MolcCache.to_device(names)``: the raw records of many entries copied
   (one slice per entry) into one pinned buffer, one host->device copy, then
-  decoded and typed on the device: (natoms, 3) f32 coordinates, type index,
-  radius and per-entry offsets -- no per-atom host work at all.
+  decoded and typed on the device by ``gm_molc_decode`` (csrc/molc.cu):
+  (natoms, 3) f32 coordinates, type index, radius and per-entry offsets -- no
+  per-atom host work at all.
 
 Layout (little-endian): "MOLC", u32 version 1, u64 count, entries (u16 name
 length, UTF-8 name, u32 natoms, natoms x (u8 element, 3 x f32)), index
@@ -147,38 +148,58 @@ class MolcCache:
 
     def to_device(self, names, device="cuda"):
         """Raw records of ``names`` -> one pinned buffer -> one H2D copy ->
-        device decode + typing.  Returns a dict of CUDA tensors: ``coords``
-        (A, 3) f32, ``type_index`` (A,) int32, ``radius`` (A,) f32 and
-        ``offsets`` (len(names)+1,) int64 (entry e owns atoms
-        [offsets[e], offsets[e+1]) after dropping untyped atoms)."""
+        decode + typing on the device (``gm_molc_decode``: three sm_100a
+        kernels, in-order compaction of the kept atoms).  Returns a dict of
+        CUDA tensors: ``coords`` (A, 3) f32, ``type_index`` (A,) int32,
+        ``radius`` (A,) f32 and ``offsets`` (len(names)+1,) int64 (entry e owns
+        atoms [offsets[e], offsets[e+1]) after dropping untyped atoms)."""
         import torch
 
+        from . import _native
+        from .packing import on_device, stream_handle
+
+        dev = torch.device(device)
         spans = [self._span(n) for n in names]
         counts = np.array([n for _, n in spans], np.int64)
         total = int(counts.sum())
-        pinned = torch.empty(max(total, 1) * ATOM_DTYPE.itemsize, dtype=torch.uint8,
+        starts = np.zeros(len(names) + 1, np.int64)
+        np.cumsum(counts, out=starts[1:])
+        hdr = starts.nbytes
+        pinned = torch.empty(hdr + max(total, 1) * ATOM_DTYPE.itemsize, dtype=torch.uint8,
                              pin_memory=True)
         host = pinned.numpy()
-        pos = 0
+        host[:hdr] = starts.view(np.uint8)
+        pos = hdr
         for off, n in spans:  # one slice copy per entry
             nb = n * ATOM_DTYPE.itemsize
             host[pos:pos + nb] = self._buf[off:off + nb]
             pos += nb
-        raw = pinned.to(device, non_blocking=True)[:total * ATOM_DTYPE.itemsize].view(total, 13)
-        table = torch.from_numpy(self._types.astype(np.int32)).to(device)
-        radii = torch.from_numpy(TYPE_RADII).to(device)
-        t = table[raw[:, 0].long()]
-        keep = t >= 0
-        xyz = raw[:, 1:13].contiguous().view(torch.float32).view(total, 3)
-        entry = torch.repeat_interleave(torch.arange(len(names), device=device),
-                                        torch.from_numpy(counts).to(device))
-        kept_per_entry = torch.zeros(len(names), dtype=torch.int64, device=device)
-        kept_per_entry.index_add_(0, entry[keep], torch.ones_like(entry[keep]))
-        offsets = torch.zeros(len(names) + 1, dtype=torch.int64, device=device)
-        offsets[1:] = torch.cumsum(kept_per_entry, 0)
-        ti = t[keep]
-        return {"coords": xyz[keep], "type_index": ti, "radius": radii[ti.long()],
-                "offsets": offsets}
+        buf = pinned.to(dev, non_blocking=True)
+        table, radii = self._device_tables(dev)
+        coords = torch.empty((max(total, 1), 3), dtype=torch.float32, device=dev)
+        type_index = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        radius = torch.empty(max(total, 1), dtype=torch.float32, device=dev)
+        offsets = torch.empty(len(names) + 1, dtype=torch.int64, device=dev)
+        with on_device(dev):
+            _native.check(_native.lib().gm_molc_decode(
+                buf.data_ptr() + hdr, buf.data_ptr(), len(names), table.data_ptr(),
+                radii.data_ptr(), coords.data_ptr(), type_index.data_ptr(), radius.data_ptr(),
+                offsets.data_ptr(), stream_handle(dev)))
+        kept = int(offsets[-1].item())  # the outputs' length (one 8-byte read back)
+        return {"coords": coords[:kept], "type_index": type_index[:kept],
+                "radius": radius[:kept], "offsets": offsets}
+
+    def _device_tables(self, dev):
+        """The element -> type table (int16) and the type radii on ``dev``,
+        uploaded once per device."""
+        import torch
+
+        cache = self.__dict__.setdefault("_dev_tables", {})
+        key = str(dev)
+        if key not in cache:
+            cache[key] = (torch.from_numpy(self._types.astype(np.int16)).to(dev),
+                          torch.from_numpy(TYPE_RADII).to(dev))
+        return cache[key]
 
     def names(self) -> list:
         return sorted(self._index)
