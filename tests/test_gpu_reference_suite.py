@@ -8,7 +8,6 @@ default shape 191-207, determinism 351-389, transform suite 392-411).
 The checker is the independent all-pairs oracle (oracle/allpairs.py).
 """
 
-
 import numpy as np
 import pytest
 
