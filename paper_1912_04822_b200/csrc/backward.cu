@@ -155,8 +155,9 @@ __device__ __forceinline__ void store_coord(const BwdArgs &P, int a, int lane, d
 // One warp per atom, flattened walk (index and vector types).
 //
 // The atom's box is cut into sub-boxes of <= kTab voxels per axis and chunks
-// of <= kRows (i, j) rows.  Phase 1: lanes compute each row's k span inside
-// the cutoff sphere and a warp scan lays the non-empty rows out back to back
+// of <= kIRows / kRows (i, j) rows (index / vector walk).  Phase 1: lanes
+// compute each row's k span inside the cutoff sphere and a warp scan lays the
+// non-empty rows out back to back
 // (row table in shared memory: start offset, k origin, b2 = dx^2 + dy^2, dx,
 // dy, Gaussian factor Ex*Ey).  Phase 2: the warp walks the flattened list in
 // windows of 32 voxels, kU windows per step -- every lane has a voxel (no
@@ -169,7 +170,14 @@ __device__ __forceinline__ void store_coord(const BwdArgs &P, int a, int lane, d
 #endif
 constexpr int kBwdWarps = GM_BWD_WARPS;
 #ifndef GM_BWD_ROWS
-#define GM_BWD_ROWS 96
+// rows per chunk of the index walk: two phase-1 passes of 32 rows exactly
+// (GM_BWD_P1X2), and 4.9 KB of shared memory per warp lets all 32 one-warp CTAs
+// reside.  C2 / C5 backward: 48 rows 100.6 / 458 us, 64 92.6 / 433, 72 96.6 /
+// 454, 80 96.0 / 446, 88 94.5 / 441, 96 94.5 / 435, 128 94.7 / 433, 192 106 / 455
+#define GM_BWD_ROWS 64
+#endif
+#ifndef GM_BWDV_ROWS
+#define GM_BWDV_ROWS 96  // rows per chunk of the vector walk (64: C4 backward 303.5 -> 305.6 us)
 #endif
 #ifndef GM_BWD_KU
 #define GM_BWD_KU 4
@@ -230,7 +238,8 @@ __device__ __forceinline__ float ld_gg(const float *p) {
     return v;
 }
 
-constexpr int kRows = GM_BWD_ROWS;  // rows per chunk
+constexpr int kRows = GM_BWDV_ROWS;  // rows per chunk (vector walk)
+constexpr int kIRows = GM_BWD_ROWS;  // rows per chunk (index walk)
 constexpr int kTab = 32;      // table entries per axis (sub-box edge)
 constexpr int kU = GM_BWD_KU;  // 32-voxel windows per step (loads in flight per lane)
 
@@ -393,8 +402,8 @@ static_assert(sizeof(IRow) == 48, "IRow must be 48 bytes");
 struct WarpIdx {
     double2 zt[kTab];  // per k: offset z - (o + k res), Gaussian factor Ez
     double dx[kTab], ex[kTab], dy[kTab], ey[kTab];
-    IRow rows[kRows];
-    unsigned starts[kRows * kTab / 32 + kU];  // bit v: a row starts at flattened voxel v
+    IRow rows[kIRows];
+    unsigned starts[kIRows * kTab / 32 + kU];  // bit v: a row starts at flattened voxel v
 };
 
 __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(const BwdArgs P) {
@@ -450,10 +459,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, GM_BWD_MINB) k_backward_index(
                     const float inv_nj = __frcp_rn((float)nj);
                     const unsigned sbase = (unsigned)((si * D + sj) * D + sk);
                     const int nrows_all = ni * nj;
-                    for (int rb = 0; rb < nrows_all; rb += kRows) {
+                    for (int rb = 0; rb < nrows_all; rb += kIRows) {
                         // ---- phase 1: row spans, compacted with a warp scan ----
                         int nrow = 0, total = 0;
-                        const int rend = min(nrows_all, rb + kRows);
+                        const int rend = min(nrows_all, rb + kIRows);
                         const int nwords = ((rend - rb) * nk + 31) >> 5;
                         for (int w = lane; w < nwords + kU; w += 32) W.starts[w] = 0u;
                         __syncwarp();
