@@ -225,6 +225,121 @@ __device__ __forceinline__ void stage_items(const FwdItem *src, FwdItem *dst, in
         : "memory");
 }
 
+// Phase B of one visit: every lane scatters its (row, column) voxels of the
+// item planned in slot *sp into plane i of the accumulator (accp).
+template <bool BINARY, bool VECTOR, bool RESL>
+__device__ __forceinline__ void scatter_visit(const FwdArgs &A, float *accp, const Slot *sp, int lane,
+                                              int i, double ox, double oy, double oz) {
+    const int D = A.D;
+    const double res = A.res;
+    const float resf = A.resf, resl = A.resl;
+    const float4 S0 = *reinterpret_cast<const float4 *>(&sp->yh);
+    const float4 S1 = *reinterpret_cast<const float4 *>(&sp->dx2);
+    const float4 S2 = *reinterpret_cast<const float4 *>(&sp->qa);
+    const int4 S3 = *reinterpret_cast<const int4 *>(&sp->arow);
+    const int jr0 = box_lo(__float_as_int(S2.z)), nj = box_hi(__float_as_int(S2.z));
+    const int kr0 = box_lo(__float_as_int(S2.w)), nk = box_hi(__float_as_int(S2.w));
+    const int nks = S3.y;
+    const float inv = __int_as_float(S3.w);  // 1/nks (approximate, exact enough)
+    const int r = small_div(lane, inv), rpi = small_div(32, inv);
+    if (BINARY) {
+        // _kernels.py:87-98 (index) / 180-192 (vector): the occupancy test
+        // d^2 <= r^2 decided like the reference's f64 expression.  The f32
+        // distance from the hi/lo offsets is within ~1e-5 A^2 of it, so
+        // outside a band of 1e-4 (r^2 + 1 A^2) around r^2 its answer is
+        // the reference's; inside the band (rare) the exact f64
+        // expression, same association, no contraction, decides.
+        const float w = S2.y;
+        const float r2f = S1.w * S1.w;  // cut = r in binary mode
+        const float band = 1e-4f * (r2f + 1.0f);
+        const float lo2 = r2f - band, hi2 = r2f + band;
+        for (int kb = 0; kb < nk; kb += 32) {
+            const int nkb = min(32, nk - kb);
+            const float invb = __frcp_rn((float)nkb);
+            const int rpb = small_div(32, invb);
+            const int rr = small_div(lane, invb), kk = kb + lane - rr * nkb;
+            if (rr >= rpb) continue;
+            const float fk = (float)(kr0 + kk);
+            const float dzf = fmaf(fk, resf, S0.z) + fmaf(fk, resl, S0.w);
+            const float b2f = fmaf(dzf, dzf, S1.x);
+            float *ap = accp + S3.x + kr0 + kk + (size_t)rr * D;
+            for (int jj = rr; jj < nj; jj += rpb, ap += (size_t)rpb * D) {
+                const float jf = (float)(jr0 + jj);
+                const float dyf = fmaf(jf, resf, S0.x) + fmaf(jf, resl, S0.y);
+                const float d2f = fmaf(dyf, dyf, b2f);
+                bool in = d2f <= lo2;
+                if (!in && d2f <= hi2) {
+                    const BinItem bi = A.bsorted[S3.z];
+                    const int4 bx = *reinterpret_cast<const int4 *>(&A.sorted[S3.z].ibox);
+                    const double dxd =
+                        __dsub_rn(__dadd_rn(ox, __dmul_rn((double)i, res)), bi.x);
+                    const double dz = __dsub_rn(
+                        __dadd_rn(oz, __dmul_rn((double)(box_lo(bx.z) + kr0 + kk), res)), bi.z);
+                    const double dy = __dsub_rn(
+                        __dadd_rn(oy, __dmul_rn((double)(box_lo(bx.y) + jr0 + jj), res)), bi.y);
+                    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dxd, dxd), __dmul_rn(dy, dy)),
+                                                __dmul_rn(dz, dz));
+                    in = d2 <= bi.r2;
+                }
+                if (in) {
+                    if (VECTOR) *ap = fmaxf(*ap, w);
+                    else *ap = 1.0f;
+                }
+            }
+        }
+    } else if (nk <= 32) {
+        // _kernels.py:99-106: Gaussian core to d0, quadratic tail to the cutoff
+        if (r < rpi) {
+            const int kk = kr0 + lane - r * nks;
+            const float fk = (float)kk;
+            const float dz = fmaf(fk, resf, S0.z) + fmaf(fk, resl, S0.w);
+            const float b2 = fmaf(dz, dz, S1.x);
+            const float cexp = S1.y, d02 = S1.z, cut = S1.w, qa = S2.x, w = S2.y;
+            const float rpif = (float)rpi;
+            float *ap = accp + S3.x + kk + r * D;
+            const int step = rpi * D;
+            float jf = (float)(jr0 + r);
+            auto val = [&](float y) {
+                const float dy = RESL ? fmaf(y, resf, S0.x) + fmaf(y, resl, S0.y)
+                                      : fmaf(y, resf, S0.x) + S0.y;
+                const float d2 = fmaf(dy, dy, b2);
+                const float g = fast_ex2(d2 * cexp);
+                const float t2 = fmaxf(cut - fast_sqrt(d2), 0.0f);
+                return d2 <= d02 ? g : qa * t2 * t2;
+            };
+            int jj = r;
+            // two rows per iteration: both accumulator reads are
+            // issued before either write (different rows)
+            for (; jj + rpi < nj; jj += 2 * rpi, jf += 2.0f * rpif, ap += 2 * step) {
+                const float v0 = val(jf), v1 = val(jf + rpif);
+                const float a0 = ap[0], a1 = ap[step];
+                ap[0] = fmaf(w, v0, a0);
+                ap[step] = fmaf(w, v1, a1);
+            }
+            if (jj < nj) *ap = fmaf(w, val(jf), *ap);
+        }
+    } else {
+        // > 32 columns (very fine grids): one row pass per 32 columns
+        const float cexp = S1.y, d02 = S1.z, cut = S1.w, qa = S2.x, w = S2.y;
+        for (int kb = lane; kb < nk; kb += 32) {
+            const int kk = kr0 + kb;
+            const float fk = (float)kk;
+            const float dz = fmaf(fk, resf, S0.z) + fmaf(fk, resl, S0.w);
+            const float b2 = fmaf(dz, dz, S1.x);
+            float *ap = accp + S3.x + kk;
+            for (int jj = 0; jj < nj; jj++, ap += D) {
+                const float jf = (float)(jr0 + jj);
+                const float dy = fmaf(jf, resf, S0.x) + fmaf(jf, resl, S0.y);
+                const float d2 = fmaf(dy, dy, b2);
+                const float g = fast_ex2(d2 * cexp);
+                const float t2 = fmaxf(cut - fast_sqrt(d2), 0.0f);
+                const float v = d2 <= d02 ? g : qa * t2 * t2;
+                *ap = fmaf(w, v, *ap);
+            }
+        }
+    }
+}
+
 template <bool BINARY, bool VECTOR, bool RESL>
 __device__ __forceinline__ void scatter_items(const FwdArgs &A, float *accp, Slot *slots, int lane,
                                               int e, int i, int jg0, int jg1, int j0, int cs,
@@ -299,111 +414,7 @@ __device__ __forceinline__ void scatter_items(const FwdArgs &A, float *accp, Slo
         while (m) {
             const int t = __ffs(m) - 1;
             m &= m - 1;
-            const float4 S0 = *reinterpret_cast<const float4 *>(&slots[t].yh);
-            const float4 S1 = *reinterpret_cast<const float4 *>(&slots[t].dx2);
-            const float4 S2 = *reinterpret_cast<const float4 *>(&slots[t].qa);
-            const int4 S3 = *reinterpret_cast<const int4 *>(&slots[t].arow);
-            const int jr0 = box_lo(__float_as_int(S2.z)), nj = box_hi(__float_as_int(S2.z));
-            const int kr0 = box_lo(__float_as_int(S2.w)), nk = box_hi(__float_as_int(S2.w));
-            const int nks = S3.y;
-            const float inv = __int_as_float(S3.w);  // 1/nks (approximate, exact enough)
-            const int r = small_div(lane, inv), rpi = small_div(32, inv);
-            if (BINARY) {
-                // _kernels.py:87-98 (index) / 180-192 (vector): the occupancy test
-                // d^2 <= r^2 decided like the reference's f64 expression.  The f32
-                // distance from the hi/lo offsets is within ~1e-5 A^2 of it, so
-                // outside a band of 1e-4 (r^2 + 1 A^2) around r^2 its answer is
-                // the reference's; inside the band (rare) the exact f64
-                // expression, same association, no contraction, decides.
-                const float w = S2.y;
-                const float r2f = S1.w * S1.w;  // cut = r in binary mode
-                const float band = 1e-4f * (r2f + 1.0f);
-                const float lo2 = r2f - band, hi2 = r2f + band;
-                for (int kb = 0; kb < nk; kb += 32) {
-                    const int nkb = min(32, nk - kb);
-                    const float invb = __frcp_rn((float)nkb);
-                    const int rpb = small_div(32, invb);
-                    const int rr = small_div(lane, invb), kk = kb + lane - rr * nkb;
-                    if (rr >= rpb) continue;
-                    const float fk = (float)(kr0 + kk);
-                    const float dzf = fmaf(fk, resf, S0.z) + fmaf(fk, resl, S0.w);
-                    const float b2f = fmaf(dzf, dzf, S1.x);
-                    float *ap = accp + S3.x + kr0 + kk + (size_t)rr * D;
-                    for (int jj = rr; jj < nj; jj += rpb, ap += (size_t)rpb * D) {
-                        const float jf = (float)(jr0 + jj);
-                        const float dyf = fmaf(jf, resf, S0.x) + fmaf(jf, resl, S0.y);
-                        const float d2f = fmaf(dyf, dyf, b2f);
-                        bool in = d2f <= lo2;
-                        if (!in && d2f <= hi2) {
-                            const BinItem bi = A.bsorted[S3.z];
-                            const int4 bx = *reinterpret_cast<const int4 *>(&A.sorted[S3.z].ibox);
-                            const double dxd =
-                                __dsub_rn(__dadd_rn(ox, __dmul_rn((double)i, res)), bi.x);
-                            const double dz = __dsub_rn(
-                                __dadd_rn(oz, __dmul_rn((double)(box_lo(bx.z) + kr0 + kk), res)), bi.z);
-                            const double dy = __dsub_rn(
-                                __dadd_rn(oy, __dmul_rn((double)(box_lo(bx.y) + jr0 + jj), res)), bi.y);
-                            const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dxd, dxd), __dmul_rn(dy, dy)),
-                                                        __dmul_rn(dz, dz));
-                            in = d2 <= bi.r2;
-                        }
-                        if (in) {
-                            if (VECTOR) *ap = fmaxf(*ap, w);
-                            else *ap = 1.0f;
-                        }
-                    }
-                }
-            } else if (nk <= 32) {
-                // _kernels.py:99-106: Gaussian core to d0, quadratic tail to the cutoff
-                if (r < rpi) {
-                    const int kk = kr0 + lane - r * nks;
-                    const float fk = (float)kk;
-                    const float dz = fmaf(fk, resf, S0.z) + fmaf(fk, resl, S0.w);
-                    const float b2 = fmaf(dz, dz, S1.x);
-                    const float cexp = S1.y, d02 = S1.z, cut = S1.w, qa = S2.x, w = S2.y;
-                    const float rpif = (float)rpi;
-                    float *ap = accp + S3.x + kk + r * D;
-                    const int step = rpi * D;
-                    float jf = (float)(jr0 + r);
-                    auto val = [&](float y) {
-                        const float dy = RESL ? fmaf(y, resf, S0.x) + fmaf(y, resl, S0.y)
-                                              : fmaf(y, resf, S0.x) + S0.y;
-                        const float d2 = fmaf(dy, dy, b2);
-                        const float g = fast_ex2(d2 * cexp);
-                        const float t2 = fmaxf(cut - fast_sqrt(d2), 0.0f);
-                        return d2 <= d02 ? g : qa * t2 * t2;
-                    };
-                    int jj = r;
-                    // two rows per iteration: both accumulator reads are
-                    // issued before either write (different rows)
-                    for (; jj + rpi < nj; jj += 2 * rpi, jf += 2.0f * rpif, ap += 2 * step) {
-                        const float v0 = val(jf), v1 = val(jf + rpif);
-                        const float a0 = ap[0], a1 = ap[step];
-                        ap[0] = fmaf(w, v0, a0);
-                        ap[step] = fmaf(w, v1, a1);
-                    }
-                    if (jj < nj) *ap = fmaf(w, val(jf), *ap);
-                }
-            } else {
-                // > 32 columns (very fine grids): one row pass per 32 columns
-                const float cexp = S1.y, d02 = S1.z, cut = S1.w, qa = S2.x, w = S2.y;
-                for (int kb = lane; kb < nk; kb += 32) {
-                    const int kk = kr0 + kb;
-                    const float fk = (float)kk;
-                    const float dz = fmaf(fk, resf, S0.z) + fmaf(fk, resl, S0.w);
-                    const float b2 = fmaf(dz, dz, S1.x);
-                    float *ap = accp + S3.x + kk;
-                    for (int jj = 0; jj < nj; jj++, ap += D) {
-                        const float jf = (float)(jr0 + jj);
-                        const float dy = fmaf(jf, resf, S0.x) + fmaf(jf, resl, S0.y);
-                        const float d2 = fmaf(dy, dy, b2);
-                        const float g = fast_ex2(d2 * cexp);
-                        const float t2 = fmaxf(cut - fast_sqrt(d2), 0.0f);
-                        const float v = d2 <= d02 ? g : qa * t2 * t2;
-                        *ap = fmaf(w, v, *ap);
-                    }
-                }
-            }
+            scatter_visit<BINARY, VECTOR, RESL>(A, accp, slots + t, lane, i, ox, oy, oz);
             __syncwarp();
         }
     }
@@ -562,6 +573,7 @@ __global__ void __launch_bounds__(kThreads, GM_FWD_MINB) k_forward(const FwdArgs
                 __stcs(obase + pp * plane + q, acc[(size_t)pp * TJ * D + q]);
     }
 }
+
 
 struct FwdConfig {
     int TI, TJ, wpp, rpw;
