@@ -107,8 +107,11 @@ __host__ __device__ inline int plane_bucket(int i, int D) { return (int)(((long 
 // on fine grids (96^3: forward -30 us) and vector typing (3.5 items per atom:
 // -20 us per step), not on 48^3 index grids (the forward saves what the pass
 // costs) -- there the items stay in item order.
+#ifndef GM_PLANE_SORT_MIND
+#define GM_PLANE_SORT_MIND 64  // index typing: plane-sort grids above this size
+#endif
 inline bool use_plane_sort(const gm_params *p, const gm_batch *b) {
-    return GM_PLANE_SORT && (p->npts > 64 || b->vector_mode);
+    return GM_PLANE_SORT && (p->npts > GM_PLANE_SORT_MIND || b->vector_mode);
 }
 
 // ---------------------------------------------------------------------------
