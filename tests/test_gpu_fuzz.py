@@ -36,7 +36,7 @@ def _random_case(seed):
     cfg["radius_type_indexed"] = bool(vector and rng.random() < 0.5)
     nex = int(rng.integers(1, 6))
     nsets = int(rng.integers(1, 4))
-    T = [int(rng.integers(1, 9)) for _ in range(nsets)]
+    T = [int(rng.integers(1, int(os.environ.get("GM_FUZZ_MAXT", "8")) + 1)) for _ in range(nsets)]
     exs = []
     for _ in range(nex):
         sets = []
@@ -63,7 +63,9 @@ def _random_case(seed):
     return cfg, exs, aug
 
 
-# GM_FUZZ_CASES widens the sweep (exploratory runs); the suite runs 40 cases
+# GM_FUZZ_CASES widens the sweep (exploratory runs; the suite runs 40 cases) and
+# GM_FUZZ_MAXT the types per set (default 8; 24 exercises the per-channel vector
+# backward beyond 16 channels: 300 + 300 cases passed at 24)
 @pytest.mark.parametrize("seed", range(int(os.environ.get("GM_FUZZ_CASES", "40"))))
 def test_random_configuration_vs_oracle(seed):
     from paper_1912_04822_b200 import GridMaker
