@@ -272,6 +272,41 @@ gm_status gm_backward_vector_host(double *coord_grad, double *type_grad, const d
                                   const double *type_radii, int32_t radius_type_indexed,
                                   const double *origin, double res, double grm, double rmult);
 
+/* ---- host packing of an index-typed batch ----
+ *
+ * GridMaker._run_batch's CSR packing (voxelizer.py:372-435) plus this
+ * library's static grouping, slot records and backward launch order, written
+ * by one native pass into the caller's image of a gm_batch (e.g. the pinned
+ * buffer it then copies to the device once).  sets: in example order; each
+ * set's coords (n,3) f32, radii (n) f32 (unscaled), type_index (n) int64 in
+ * [0, num_types).  centers: (nexamples,3) f64 default centers (launch-order
+ * key only).  layout: byte offsets into dst of each array (sizes: atoms,
+ * sets, nexamples, nexamples*(nchannels+1), segs nexamples*nchannels at most;
+ * bwd_slot -1 = no launch order).  bwd_order: 0 atom order, 1 slab order.
+ * Writes info (natoms, groups with items, largest group, largest example). */
+typedef struct {
+    const float *coords;
+    const float *radii;
+    const int64_t *type_index;
+    int64_t n;
+    int32_t example, num_types;
+} gm_pack_set;
+
+typedef struct {
+    int64_t coords32, atom_radius, atom_set, atom_type, set_start, set_end, set_example,
+        set_choff, set_t, bwd_slot, ex_item_start, ex_item_end, item_perm, chan_off, segs,
+        slot_rec;
+} gm_pack_layout;
+
+typedef struct {
+    int32_t natoms, nsegs, max_seg_items, max_example_items;
+} gm_pack_info;
+
+gm_status gm_pack_index_host(const gm_pack_set *sets, int32_t nsets, int32_t nexamples,
+                             int32_t nchannels, double radius_scale, const double *centers,
+                             int32_t bwd_order, uint8_t *dst, const gm_pack_layout *layout,
+                             gm_pack_info *info);
+
 /* ---- MOLC cache records -> typed atoms ----
  *
  * Replaces the reference's per-atom decode and typing of a cache entry
@@ -303,7 +338,8 @@ gm_status gm_draw_transforms(const double *u, int64_t n, int32_t rotation, doubl
 const char *gm_last_error(void);
 const char *gm_version(void);
 int32_t gm_device_count(void);
-/* sizeof(gm_params) (which = 0), gm_batch (1), gm_dataset (2) or gm_capacity (3): ABI check. */
+/* sizeof(gm_params) (which = 0), gm_batch (1), gm_dataset (2), gm_capacity (3),
+ * gm_pack_set (4), gm_pack_layout (5) or gm_pack_info (6): ABI check. */
 int32_t gm_struct_size(int32_t which);
 /* Kernel launches issued by this process since the last reset (bench evidence). */
 int64_t gm_launch_count(int32_t reset);

@@ -88,6 +88,31 @@ class GmCapacity(ctypes.Structure):
                 ("weights", _c_int32), ("type_radii", _c_int32), ("jobs", _c_int32)]
 
 
+class GmPackSet(ctypes.Structure):
+    """Mirror of ``gm_pack_set``."""
+
+    _fields_ = [("coords", _vp), ("radii", _vp), ("type_index", _vp), ("n", _c_int64),
+                ("example", _c_int32), ("num_types", _c_int32)]
+
+
+PACK_ARRAYS = ("coords32", "atom_radius", "atom_set", "atom_type", "set_start", "set_end",
+               "set_example", "set_choff", "set_t", "bwd_slot", "ex_item_start", "ex_item_end",
+               "item_perm", "chan_off", "segs", "slot_rec")
+
+
+class GmPackLayout(ctypes.Structure):
+    """Mirror of ``gm_pack_layout`` (byte offsets, -1 = absent)."""
+
+    _fields_ = [(name, _c_int64) for name in PACK_ARRAYS]
+
+
+class GmPackInfo(ctypes.Structure):
+    """Mirror of ``gm_pack_info``."""
+
+    _fields_ = [("natoms", _c_int32), ("nsegs", _c_int32), ("max_seg_items", _c_int32),
+                ("max_example_items", _c_int32)]
+
+
 _LIB = None
 INLINE_MAX_EXAMPLES = 200  # GM_INLINE_MAX_EXAMPLES
 
@@ -98,6 +123,7 @@ EXPORTS = (
     "gm_launch_count", "gm_struct_size", "gm_draw_transforms", "gm_forward_jobs",
     "gm_assemble",
     "gm_molc_decode",
+    "gm_pack_index_host",
 )
 
 
@@ -147,6 +173,9 @@ def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     L.gm_assemble.argtypes = [P(GmParams), P(GmDataset), _vp, _c_int32, P(GmBatch),
                               P(GmCapacity), _vp, _vp]
     L.gm_assemble.restype = ctypes.c_int
+    L.gm_pack_index_host.argtypes = [P(GmPackSet), _c_int32, _c_int32, _c_int32, _c_double,
+                                     _vp, _c_int32, _vp, P(GmPackLayout), P(GmPackInfo)]
+    L.gm_pack_index_host.restype = ctypes.c_int
     L.gm_molc_decode.argtypes = [_vp, _vp, _c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
     L.gm_molc_decode.restype = ctypes.c_int
     L.gm_draw_transforms.argtypes = [_vp, _c_int64, _c_int32, _c_double, _vp, _vp]
@@ -159,7 +188,10 @@ def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     if L.gm_struct_size(0) != ctypes.sizeof(GmParams) or \
             L.gm_struct_size(1) != ctypes.sizeof(GmBatch) or \
             L.gm_struct_size(2) != ctypes.sizeof(GmDataset) or \
-            L.gm_struct_size(3) != ctypes.sizeof(GmCapacity):
+            L.gm_struct_size(3) != ctypes.sizeof(GmCapacity) or \
+            L.gm_struct_size(4) != ctypes.sizeof(GmPackSet) or \
+            L.gm_struct_size(5) != ctypes.sizeof(GmPackLayout) or \
+            L.gm_struct_size(6) != ctypes.sizeof(GmPackInfo):
         raise DeviceError("ABI mismatch between _native.py and libgridmaker_b200.so")
     L.gm_launch_count.argtypes = [_c_int32]
     L.gm_launch_count.restype = _c_int64

@@ -681,6 +681,9 @@ extern "C" int32_t gm_struct_size(int32_t which) {
            : which == 1 ? (int32_t)sizeof(gm_batch)
            : which == 2 ? (int32_t)sizeof(gm_dataset)
            : which == 3 ? (int32_t)sizeof(gm_capacity)
+           : which == 4 ? (int32_t)sizeof(gm_pack_set)
+           : which == 5 ? (int32_t)sizeof(gm_pack_layout)
+           : which == 6 ? (int32_t)sizeof(gm_pack_info)
                         : -1;
 }
 extern "C" int64_t gm_launch_count(int32_t reset) {

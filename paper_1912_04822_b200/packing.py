@@ -28,6 +28,9 @@ from . import errors
 _ALIGN = 256
 # GM_NO_JOBS=1: dense forward launch (A/B timing of the job table)
 _NO_JOBS = os.environ.get("GM_NO_JOBS", "") not in ("", "0")
+# GM_PACK=numpy: index-typed batches packed by the numpy code below instead of
+# the native packer (gm_pack_index_host); the two are compared in the tests
+_NATIVE_PACK = os.environ.get("GM_PACK", "native") != "numpy"
 
 
 class _Layout:
@@ -41,6 +44,13 @@ class _Layout:
         self.offsets[name] = (self.size, arr.dtype, arr.shape)
         self.arrays.append((name, arr))
         self.size += (arr.nbytes + _ALIGN - 1) // _ALIGN * _ALIGN if arr.nbytes else _ALIGN
+
+    def reserve(self, name, dtype, shape):
+        """Room for an array another writer fills in place (the native packer)."""
+        dtype = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dtype.itemsize
+        self.offsets[name] = (self.size, dtype, tuple(shape))
+        self.size += (nbytes + _ALIGN - 1) // _ALIGN * _ALIGN if nbytes else _ALIGN
 
 
 class PackedBatch:
@@ -70,6 +80,9 @@ class PackedBatch:
             starts[1:] = np.cumsum(counts)[:-1]
         self.natoms = int(counts.sum())
         scale = float(radius_scale)
+        if not self.vector_mode and _NATIVE_PACK and (_BWD_ORDER in ("slab", "none")):
+            self._pack_index_native(example_sets, placed, counts, starts, scale)
+            return
 
         coords = np.zeros((self.natoms, 3), np.float32)
         radius = np.zeros(self.natoms, np.float64)
@@ -230,9 +243,12 @@ class PackedBatch:
         for name, arr in L.arrays:
             off = L.offsets[name][0]
             hb[off:off + arr.nbytes] = arr.reshape(-1).view(np.uint8)
-        self.dev = torch.empty(L.size, dtype=torch.uint8, device=self.device)
-        self.upload()
+        self._to_device(L.size)
 
+    def _to_device(self, size) -> None:
+        """The device mirror of the host image (one H2D copy) and the workspace."""
+        self.dev = torch.empty(size, dtype=torch.uint8, device=self.device)
+        self.upload()
         nbytes = _native.lib().gm_workspace_bytes(max(self.natoms, 1), max(self.nitems, 1),
                                                    max(self.nexamples, 1), self.nchannels)
         self.workspace = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
@@ -241,6 +257,71 @@ class PackedBatch:
         self._stage = None
         self._gm = None
         self._gm_ref = None
+
+    def _pack_index_native(self, example_sets, placed, counts, starts, scale) -> None:
+        """Index typing: every packed array written in place, into the pinned
+        host image, by the native packer (gm_pack_index_host, csrc/pack.cu) --
+        the same arrays as the numpy packing (tested array for array; the
+        backward launch order is a permutation with the same slab grouping)."""
+        N, C, S, A = self.nexamples, self.nchannels, self.nsets, self.natoms
+        self.default_centers = np.stack([_default_center(sets) for sets in example_sets]) \
+            if N else np.zeros((0, 3))
+        order = _BWD_ORDER == "slab" and A > 0
+        L = _Layout()
+        L.reserve("coords32", np.float32, (A, 3))
+        L.reserve("atom_radius", np.float64, (A,))
+        L.reserve("atom_set", np.int32, (A,))
+        for name in ("set_start", "set_end", "set_example", "set_choff", "set_t"):
+            L.reserve(name, np.int32, (S,))
+        L.reserve("atom_type", np.int32, (A,))
+        if order:
+            L.reserve("bwd_slot", np.int32, (A,))
+        L.reserve("ex_item_start", np.int32, (N,))
+        L.reserve("ex_item_end", np.int32, (N,))
+        L.reserve("item_perm", np.int32, (A,))
+        L.reserve("chan_off", np.int32, (N * (C + 1),))
+        L.reserve("segs", np.int32, (N * C,))  # capacity; the groups with items come first
+        if A:
+            L.reserve("slot_rec", np.uint8, (48 * A,))
+        self.host = torch.empty(L.size, dtype=torch.uint8, pin_memory=self.device.type == "cuda")
+        layout = _native.GmPackLayout(*[L.offsets[n][0] if n in L.offsets else -1
+                                        for n in _native.PACK_ARRAYS])
+        sets_c = (_native.GmPackSet * max(S, 1))()
+        keep = []
+        for s, (e, _, cs) in enumerate(placed):
+            ps = sets_c[s]
+            n = int(counts[s])
+            ps.n, ps.example, ps.num_types = n, e, int(cs.num_types)
+            if n:
+                arrs = (np.ascontiguousarray(cs.coords, np.float32),
+                        np.ascontiguousarray(cs.radii, np.float32),
+                        np.ascontiguousarray(cs.type_index, np.int64))
+                keep.append(arrs)
+                ps.coords, ps.radii, ps.type_index = (a.ctypes.data for a in arrs)
+        centers = np.ascontiguousarray(self.default_centers, np.float64)
+        info = _native.GmPackInfo()
+        _native.check(_native.lib().gm_pack_index_host(
+            sets_c, S, N, C, scale, centers.ctypes.data if N else None, int(order),
+            self.host.data_ptr(), ctypes.byref(layout), ctypes.byref(info)))
+        off = L.offsets["segs"][0]
+        L.offsets["segs"] = (off, np.dtype(np.int32), (int(info.nsegs),))
+        self.offsets = L.offsets
+        self.nsegs, self.max_seg_items = int(info.nsegs), int(info.max_seg_items)
+        self.max_example_items = int(info.max_example_items)
+        self.nitems, self.nweights = A, 0
+
+        hb = self.host.numpy()
+
+        def view(name):
+            o, dt, shape = L.offsets[name]
+            n = int(np.prod(shape))
+            return hb[o:o + n * dt.itemsize].view(dt).reshape(shape)
+
+        set_example = view("set_example")
+        self.atom_example = set_example[view("atom_set")] if A else np.zeros(0, np.int32)
+        self._bwd_slot_host = view("bwd_slot") if order else None
+        self.placed = [(e, choff, cs, int(starts[s]), -1) for s, (e, choff, cs) in enumerate(placed)]
+        self._to_device(L.size)
 
     # ------------------------------------------------------------------
     @property

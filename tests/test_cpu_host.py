@@ -35,6 +35,9 @@ def test_abi_struct_sizes_match_bindings():
     assert L.gm_struct_size(1) == ctypes.sizeof(_native.GmBatch)
     assert L.gm_struct_size(2) == ctypes.sizeof(_native.GmDataset)
     assert L.gm_struct_size(3) == ctypes.sizeof(_native.GmCapacity)
+    assert L.gm_struct_size(4) == ctypes.sizeof(_native.GmPackSet)
+    assert L.gm_struct_size(5) == ctypes.sizeof(_native.GmPackLayout)
+    assert L.gm_struct_size(6) == ctypes.sizeof(_native.GmPackInfo)
     assert L.gm_version().startswith(b"gridmaker_b200")
 
 
@@ -405,3 +408,70 @@ def test_thread_control_api():
     with pytest.raises(ValueError):
         set_num_threads(0)
     set_num_threads(n0)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_native_packer_equals_numpy_packing(seed, monkeypatch):
+    """gm_pack_index_host (csrc/pack.cu) writes the numpy packing's arrays:
+    every array byte for byte, except the backward launch order, which must
+    be a permutation grouping each (example, channel) slab's atoms together.
+    Odd shapes included: empty and single-atom sets, an example without atoms."""
+    import torch
+
+    import paper_1912_04822_b200.packing as packing
+    from conftest import random_coordinate_set
+    from paper_1912_04822_b200 import synthetic
+
+    rng = np.random.default_rng(seed)
+    exs = [ex.coord_sets for ex in synthetic.batch(4, seed=seed)]
+    for k in range(4):
+        exs.append([random_coordinate_set(rng, [0, 1, 7, 0][k], 14, 9.0),
+                    random_coordinate_set(rng, [5, 0, 1, 0][k], 14, 4.0)])
+    scale = [1.0, 0.7, 1.3][seed]
+
+    def build(native):
+        monkeypatch.setattr(packing, "_NATIVE_PACK", native)
+        return packing.PackedBatch(exs, 28, False, scale, False, torch.device("cpu"))
+
+    a, b = build(True), build(False)
+    for attr in ("natoms", "nsets", "nitems", "nsegs", "max_seg_items", "max_example_items"):
+        assert getattr(a, attr) == getattr(b, attr), attr
+    np.testing.assert_array_equal(a.default_centers, b.default_centers)
+    np.testing.assert_array_equal(a.atom_example, b.atom_example)
+    assert [(e, c, id(cs), a0) for e, c, cs, a0, _ in a.placed] == \
+        [(e, c, id(cs), a0) for e, c, cs, a0, _ in b.placed]
+
+    def arr(pb, name):
+        off, dt, shape = pb.offsets[name]
+        n = int(np.prod(shape))
+        return pb.host.numpy()[off:off + n * dt.itemsize].view(dt).reshape(shape)
+
+    for name in ("coords32", "atom_radius", "atom_set", "atom_type", "set_start", "set_end",
+                 "set_example", "set_choff", "set_t", "ex_item_start", "ex_item_end",
+                 "item_perm", "chan_off", "segs"):
+        np.testing.assert_array_equal(arr(a, name), arr(b, name), err_msg=name)
+    ra = arr(a, "slot_rec").view(packing._SLOT_DTYPE)
+    rb = arr(b, "slot_rec").view(packing._SLOT_DTYPE)
+    for f in ("x", "y", "z", "atom", "ch", "ex", "single", "r"):
+        np.testing.assert_array_equal(ra[f], rb[f], err_msg=f)
+    bs = arr(a, "bwd_slot")
+    assert np.array_equal(np.sort(bs), np.arange(a.natoms))
+    np.testing.assert_array_equal(ra["bslot"], bs[ra["atom"]])
+    # slab grouping: in launch order, each (example, channel) slab is contiguous
+    slab = a.atom_example.astype(np.int64) * 28 + arr(a, "set_choff")[arr(a, "atom_set")] + \
+        arr(a, "atom_type")
+    launch = slab[np.argsort(bs)]
+    assert (np.diff(launch) >= 0).all()
+
+
+def test_native_packer_without_atoms():
+    """A batch whose sets are all empty packs (no slot records, no launch order)."""
+    import torch
+
+    from conftest import random_coordinate_set
+    from paper_1912_04822_b200.packing import PackedBatch
+
+    rng = np.random.default_rng(0)
+    exs = [[random_coordinate_set(rng, 0, 3, 4.0), random_coordinate_set(rng, 0, 2, 4.0)]] * 2
+    pb = PackedBatch(exs, 5, False, 1.0, False, torch.device("cpu"))
+    assert pb.natoms == 0 and pb.nsegs == 0 and "slot_rec" not in pb.offsets
