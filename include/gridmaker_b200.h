@@ -307,6 +307,33 @@ gm_status gm_pack_index_host(const gm_pack_set *sets, int32_t nsets, int32_t nex
                              int32_t bwd_order, uint8_t *dst, const gm_pack_layout *layout,
                              gm_pack_info *info);
 
+/* The same for vector typing: each set's type_vector (n, num_types) f32 weight
+ * rows and, when radius_type_indexed, its type_radii (num_types) f32 (may be
+ * NULL otherwise).  Items = nonzero weights, atom-major then channel
+ * (_kernels.py:159-166); item_windex (nitems, host) receives each item's entry
+ * of the packed weight rows.  layout: as gm_pack_vlayout (weights nweights =
+ * sum n*num_types, type_radius sum num_types, items nitems = nonzero weights). */
+typedef struct {
+    const float *coords;
+    const float *radii;
+    const float *type_vector;
+    const float *type_radii;
+    int64_t n;
+    int32_t example, num_types;
+} gm_pack_vset;
+
+typedef struct {
+    int64_t coords32, atom_radius, atom_set, set_start, set_end, set_example, set_choff, set_t,
+        set_wstart, set_trstart, weights, type_radius, item_atom, item_channel, item_weight,
+        item_radius, bwd_slot, ex_item_start, ex_item_end, item_perm, chan_off, segs;
+} gm_pack_vlayout;
+
+gm_status gm_pack_vector_host(const gm_pack_vset *sets, int32_t nsets, int32_t nexamples,
+                              int32_t nchannels, double radius_scale, int32_t radius_type_indexed,
+                              const double *centers, int32_t bwd_order, uint8_t *dst,
+                              const gm_pack_vlayout *layout, int64_t *item_windex,
+                              gm_pack_info *info);
+
 /* ---- MOLC cache records -> typed atoms ----
  *
  * Replaces the reference's per-atom decode and typing of a cache entry
@@ -339,7 +366,8 @@ const char *gm_last_error(void);
 const char *gm_version(void);
 int32_t gm_device_count(void);
 /* sizeof(gm_params) (which = 0), gm_batch (1), gm_dataset (2), gm_capacity (3),
- * gm_pack_set (4), gm_pack_layout (5) or gm_pack_info (6): ABI check. */
+ * gm_pack_set (4), gm_pack_layout (5), gm_pack_info (6), gm_pack_vset (7) or
+ * gm_pack_vlayout (8): ABI check. */
 int32_t gm_struct_size(int32_t which);
 /* Kernel launches issued by this process since the last reset (bench evidence). */
 int64_t gm_launch_count(int32_t reset);

@@ -106,6 +106,25 @@ class GmPackLayout(ctypes.Structure):
     _fields_ = [(name, _c_int64) for name in PACK_ARRAYS]
 
 
+class GmPackVSet(ctypes.Structure):
+    """Mirror of ``gm_pack_vset``."""
+
+    _fields_ = [("coords", _vp), ("radii", _vp), ("type_vector", _vp), ("type_radii", _vp),
+                ("n", _c_int64), ("example", _c_int32), ("num_types", _c_int32)]
+
+
+PACK_VARRAYS = ("coords32", "atom_radius", "atom_set", "set_start", "set_end", "set_example",
+                "set_choff", "set_t", "set_wstart", "set_trstart", "weights", "type_radius",
+                "item_atom", "item_channel", "item_weight", "item_radius", "bwd_slot",
+                "ex_item_start", "ex_item_end", "item_perm", "chan_off", "segs")
+
+
+class GmPackVLayout(ctypes.Structure):
+    """Mirror of ``gm_pack_vlayout`` (byte offsets, -1 = absent)."""
+
+    _fields_ = [(name, _c_int64) for name in PACK_VARRAYS]
+
+
 class GmPackInfo(ctypes.Structure):
     """Mirror of ``gm_pack_info``."""
 
@@ -124,6 +143,7 @@ EXPORTS = (
     "gm_assemble",
     "gm_molc_decode",
     "gm_pack_index_host",
+    "gm_pack_vector_host",
 )
 
 
@@ -176,6 +196,10 @@ def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     L.gm_pack_index_host.argtypes = [P(GmPackSet), _c_int32, _c_int32, _c_int32, _c_double,
                                      _vp, _c_int32, _vp, P(GmPackLayout), P(GmPackInfo)]
     L.gm_pack_index_host.restype = ctypes.c_int
+    L.gm_pack_vector_host.argtypes = [P(GmPackVSet), _c_int32, _c_int32, _c_int32, _c_double,
+                                      _c_int32, _vp, _c_int32, _vp, P(GmPackVLayout), _vp,
+                                      P(GmPackInfo)]
+    L.gm_pack_vector_host.restype = ctypes.c_int
     L.gm_molc_decode.argtypes = [_vp, _vp, _c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
     L.gm_molc_decode.restype = ctypes.c_int
     L.gm_draw_transforms.argtypes = [_vp, _c_int64, _c_int32, _c_double, _vp, _vp]
@@ -191,7 +215,9 @@ def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
             L.gm_struct_size(3) != ctypes.sizeof(GmCapacity) or \
             L.gm_struct_size(4) != ctypes.sizeof(GmPackSet) or \
             L.gm_struct_size(5) != ctypes.sizeof(GmPackLayout) or \
-            L.gm_struct_size(6) != ctypes.sizeof(GmPackInfo):
+            L.gm_struct_size(6) != ctypes.sizeof(GmPackInfo) or \
+            L.gm_struct_size(7) != ctypes.sizeof(GmPackVSet) or \
+            L.gm_struct_size(8) != ctypes.sizeof(GmPackVLayout):
         raise DeviceError("ABI mismatch between _native.py and libgridmaker_b200.so")
     L.gm_launch_count.argtypes = [_c_int32]
     L.gm_launch_count.restype = _c_int64

@@ -684,6 +684,8 @@ extern "C" int32_t gm_struct_size(int32_t which) {
            : which == 4 ? (int32_t)sizeof(gm_pack_set)
            : which == 5 ? (int32_t)sizeof(gm_pack_layout)
            : which == 6 ? (int32_t)sizeof(gm_pack_info)
+           : which == 7 ? (int32_t)sizeof(gm_pack_vset)
+           : which == 8 ? (int32_t)sizeof(gm_pack_vlayout)
                         : -1;
 }
 extern "C" int64_t gm_launch_count(int32_t reset) {

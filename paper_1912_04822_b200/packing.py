@@ -80,8 +80,12 @@ class PackedBatch:
             starts[1:] = np.cumsum(counts)[:-1]
         self.natoms = int(counts.sum())
         scale = float(radius_scale)
-        if not self.vector_mode and _NATIVE_PACK and (_BWD_ORDER in ("slab", "none")):
+        if not self.vector_mode and _NATIVE_PACK and _BWD_ORDER in ("slab", "none"):
             self._pack_index_native(example_sets, placed, counts, starts, scale)
+            return
+        if self.vector_mode and _NATIVE_PACK and _BWD_ORDER in ("slab", "lpt", "lpt_local", "none"):
+            self._pack_vector_native(example_sets, placed, counts, starts, scale,
+                                     bool(radius_type_indexed))
             return
 
         coords = np.zeros((self.natoms, 3), np.float32)
@@ -257,6 +261,82 @@ class PackedBatch:
         self._stage = None
         self._gm = None
         self._gm_ref = None
+
+    def _pack_vector_native(self, example_sets, placed, counts, starts, scale, rti) -> None:
+        """Vector typing through gm_pack_vector_host (csrc/pack.cu): the
+        numpy vector packing's arrays (tested array for array), items = the
+        nonzero weights atom-major then channel, the per-example launch order."""
+        N, C, S, A = self.nexamples, self.nchannels, self.nsets, self.natoms
+        self.default_centers = np.stack([_default_center(sets) for sets in example_sets]) \
+            if N else np.zeros((0, 3))
+        sets_c = (_native.GmPackVSet * max(S, 1))()
+        keep, nitems, nweights, ntr = [], 0, 0, 0
+        self.placed = []
+        for s, (e, choff, cs) in enumerate(placed):
+            n, nt = int(counts[s]), int(cs.num_types)
+            ps = sets_c[s]
+            ps.n, ps.example, ps.num_types = n, e, nt
+            if n:
+                tv = np.ascontiguousarray(cs.type_vector, np.float32)
+                arrs = [np.ascontiguousarray(cs.coords, np.float32),
+                        np.ascontiguousarray(cs.radii, np.float32), tv]
+                if rti:
+                    if cs.type_radii is None:
+                        raise errors.ConfigError(
+                            "radius_type_indexed requires coordinate sets typed from a table "
+                            "(type_radii is missing)")
+                    arrs.append(np.ascontiguousarray(cs.type_radii, np.float32))
+                    ps.type_radii = arrs[3].ctypes.data
+                keep.append(arrs)
+                ps.coords, ps.radii, ps.type_vector = (x.ctypes.data for x in arrs[:3])
+                nitems += int(np.count_nonzero(tv))
+            self.placed.append((e, choff, cs, int(starts[s]), nweights))
+            nweights += n * nt
+            ntr += nt
+        I = nitems
+        order = A > 0 and _BWD_ORDER != "none"
+        L = _Layout()
+        L.reserve("coords32", np.float32, (A, 3))
+        L.reserve("atom_radius", np.float64, (A,))
+        L.reserve("atom_set", np.int32, (A,))
+        for name in ("set_start", "set_end", "set_example", "set_choff", "set_t"):
+            L.reserve(name, np.int32, (S,))
+        if order:
+            L.reserve("bwd_slot", np.int32, (A,))
+        L.reserve("weights", np.float32, (nweights,))
+        L.reserve("type_radius", np.float64, (ntr,))
+        L.reserve("set_wstart", np.int32, (S,))
+        L.reserve("set_trstart", np.int32, (S,))
+        for name, dt in (("item_atom", np.int32), ("item_channel", np.int32),
+                         ("item_weight", np.float32), ("item_radius", np.float64)):
+            L.reserve(name, dt, (I,))
+        L.reserve("ex_item_start", np.int32, (N,))
+        L.reserve("ex_item_end", np.int32, (N,))
+        L.reserve("item_perm", np.int32, (I,))
+        L.reserve("chan_off", np.int32, (N * (C + 1),))
+        L.reserve("segs", np.int32, (N * C,))
+        self.host = torch.empty(L.size, dtype=torch.uint8, pin_memory=self.device.type == "cuda")
+        layout = _native.GmPackVLayout(*[L.offsets[n][0] if n in L.offsets else -1
+                                         for n in _native.PACK_VARRAYS])
+        self.item_windex = np.empty(I, np.int64)
+        centers = np.ascontiguousarray(self.default_centers, np.float64)
+        info = _native.GmPackInfo()
+        _native.check(_native.lib().gm_pack_vector_host(
+            sets_c, S, N, C, scale, int(rti), centers.ctypes.data if N else None, int(order),
+            self.host.data_ptr(), ctypes.byref(layout),
+            self.item_windex.ctypes.data if I else None, ctypes.byref(info)))
+        off = L.offsets["segs"][0]
+        L.offsets["segs"] = (off, np.dtype(np.int32), (int(info.nsegs),))
+        self.offsets = L.offsets
+        self.nsegs, self.max_seg_items = int(info.nsegs), int(info.max_seg_items)
+        self.max_example_items = int(info.max_example_items)
+        self.nitems, self.nweights = I, nweights
+        hb = self.host.numpy()
+        o, dt, shape = L.offsets["atom_set"]
+        atom_set = hb[o:o + A * 4].view(np.int32)
+        set_example = np.array([p[0] for p in placed], np.int32)
+        self.atom_example = set_example[atom_set] if A else np.zeros(0, np.int32)
+        self._to_device(L.size)
 
     def _pack_index_native(self, example_sets, placed, counts, starts, scale) -> None:
         """Index typing: every packed array written in place, into the pinned

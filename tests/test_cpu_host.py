@@ -38,6 +38,8 @@ def test_abi_struct_sizes_match_bindings():
     assert L.gm_struct_size(4) == ctypes.sizeof(_native.GmPackSet)
     assert L.gm_struct_size(5) == ctypes.sizeof(_native.GmPackLayout)
     assert L.gm_struct_size(6) == ctypes.sizeof(_native.GmPackInfo)
+    assert L.gm_struct_size(7) == ctypes.sizeof(_native.GmPackVSet)
+    assert L.gm_struct_size(8) == ctypes.sizeof(_native.GmPackVLayout)
     assert L.gm_version().startswith(b"gridmaker_b200")
 
 
@@ -475,3 +477,56 @@ def test_native_packer_without_atoms():
     exs = [[random_coordinate_set(rng, 0, 3, 4.0), random_coordinate_set(rng, 0, 2, 4.0)]] * 2
     pb = PackedBatch(exs, 5, False, 1.0, False, torch.device("cpu"))
     assert pb.natoms == 0 and pb.nsegs == 0 and "slot_rec" not in pb.offsets
+
+
+@pytest.mark.parametrize("rti", [False, True])
+def test_native_vector_packer_equals_numpy_packing(rti, monkeypatch):
+    """gm_pack_vector_host writes the numpy vector packing's arrays (weights,
+    type radii, nonzero-weight items, static grouping), the same item_windex
+    and placements; its launch order keeps each example's atoms together."""
+    import torch
+
+    import paper_1912_04822_b200.packing as packing
+    from conftest import random_coordinate_set
+    from paper_1912_04822_b200 import make_vector_types, synthetic
+
+    from paper_1912_04822_b200.coordsets import CoordinateSet
+
+    rng = np.random.default_rng(4)
+    exs = [ex.coord_sets for ex in synthetic.batch(4, seed=4, vector=True)]
+    tr = synthetic.TYPE_RADII.astype(np.float32)
+
+    def odd(n):  # vector-typed set with type radii (empty / single-atom ones included)
+        v = make_vector_types(random_coordinate_set(rng, n, 14, 8.0))
+        return CoordinateSet(coords=v.coords, radii=v.radii, num_types=14,
+                             type_vector=v.type_vector, type_radii=tr)
+
+    for k in range(3):
+        exs.append([odd([0, 1, 9][k]), odd([6, 0, 1][k])])
+
+    def build(native):
+        monkeypatch.setattr(packing, "_NATIVE_PACK", native)
+        return packing.PackedBatch(exs, 28, True, 1.2, rti, torch.device("cpu"))
+
+    a, b = build(True), build(False)
+    for attr in ("natoms", "nsets", "nitems", "nweights", "nsegs", "max_seg_items",
+                 "max_example_items"):
+        assert getattr(a, attr) == getattr(b, attr), attr
+    np.testing.assert_array_equal(a.item_windex, b.item_windex)
+    np.testing.assert_array_equal(a.atom_example, b.atom_example)
+    assert [(e, c, a0, w) for e, c, _, a0, w in a.placed] == \
+        [(e, c, a0, w) for e, c, _, a0, w in b.placed]
+
+    def arr(pb, name):
+        off, dt, shape = pb.offsets[name]
+        n = int(np.prod(shape))
+        return pb.host.numpy()[off:off + n * dt.itemsize].view(dt).reshape(shape)
+
+    for name in ("coords32", "atom_radius", "atom_set", "set_start", "set_end", "set_example",
+                 "set_choff", "set_t", "set_wstart", "set_trstart", "weights", "type_radius",
+                 "item_atom", "item_channel", "item_weight", "item_radius", "ex_item_start",
+                 "ex_item_end", "item_perm", "chan_off", "segs"):
+        np.testing.assert_array_equal(arr(a, name), arr(b, name), err_msg=name)
+    bs = arr(a, "bwd_slot")
+    assert np.array_equal(np.sort(bs), np.arange(a.natoms))
+    assert (np.diff(a.atom_example[np.argsort(bs)]) >= 0).all()

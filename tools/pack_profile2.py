@@ -8,7 +8,7 @@ sys.path.insert(0, "/root/repo")
 import bench
 from paper_1912_04822_b200 import GridMaker
 
-cfg = bench.CONFIGS["c2"]
+cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
 exs, _ = bench.make_batch(cfg, 0, 1)
 gm = GridMaker()
 sets = [ex.coord_sets for ex in exs]
