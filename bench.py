@@ -369,6 +369,7 @@ def fresh_leg(args, cfg, gm, rank, ws, dev, stream, ev, barrier, out, tg, pool=1
     host_cg = [torch.empty((cap, 3), dtype=torch.float32, pin_memory=True) for _ in range(2)]
     copy_s = torch.cuda.Stream(device=dev)
     done = [torch.cuda.Event(), torch.cuda.Event()]
+    bwd_done = [torch.cuda.Event(), torch.cuda.Event()]
     nbytes = [0, 0]
 
     def step(k):
@@ -381,12 +382,11 @@ def fresh_leg(args, cfg, gm, rank, ws, dev, stream, ev, barrier, out, tg, pool=1
         stream.wait_event(done[x])  # the D2H of two steps ago has read cgs[x]
         gm.backward_packed(ab, o, reuse_prepared=True, coord_grad=cg,
                            type_grad=tg[:max(ab.nweights, 1)] if tg is not None else None)
-        ev_b = torch.cuda.Event()
-        ev_b.record(stream)
+        bwd_done[x].record(stream)
+        copy_s.wait_event(bwd_done[x])
         with torch.cuda.stream(copy_s):
-            copy_s.wait_event(ev_b)
             host_cg[x][:ab.natoms].copy_(cg, non_blocking=True)
-            done[x].record(copy_s)
+        done[x].record(copy_s)
         nbytes[0] += ab.ids.nbytes + 8 * 18 * ab.nexamples
         nbytes[1] += 12 * ab.natoms
 
