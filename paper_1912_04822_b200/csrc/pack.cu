@@ -10,6 +10,7 @@
 // straight into the caller's (pinned) image of the batch.  Same arrays as the
 // numpy packing in packing.py, byte for byte except the launch order (a
 // permutation that only affects speed).  Host code only.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
