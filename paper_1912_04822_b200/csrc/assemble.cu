@@ -12,6 +12,8 @@
 // order), writes its set rows, channel offsets and nonzero-channel list.  The
 // forward job table follows on the device (forward.cu: k_job_build).  Batch
 // sizes come from the dataset's host mirrors: no sync.
+#include <algorithm>
+#include <cstring>
 #include <type_traits>
 
 #include "common.cuh"
