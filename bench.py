@@ -337,9 +337,9 @@ def run_reference(args, cfg):
     return 0
 
 
-def fresh_leg(args, cfg, gm, rank, ws, dev, stream, ev, barrier, out, tg, pool=1000):
-    """e2e with FRESH batches: a pool of `pool` examples per rank (the first
-    batch-size of them are the headline batch) is uploaded once as a
+def fresh_leg(args, cfg, gm, rank, ws, dev, stream, ev, barrier, out, tg, exs, pool=1000):
+    """e2e with FRESH batches: a pool of `pool` examples per rank (the rank's
+    headline batch `exs`, then examples from a rank-seeded stream) is uploaded once as a
     DeviceDataset; every step draws a new shuffled index list, assembles the
     batch on the device (gm_assemble: packing + job table), draws its
     transforms, grids, back-propagates 1/2|grid|^2 and reads the coordinate
@@ -347,12 +347,14 @@ def fresh_leg(args, cfg, gm, rank, ws, dev, stream, ev, barrier, out, tg, pool=1
     PCIe are the index list and the transforms (inside the kernel launches)."""
     import torch
 
-    from paper_1912_04822_b200 import geom
+    from paper_1912_04822_b200 import geom, synthetic
     from paper_1912_04822_b200.dataset import DeviceDataset
     from paper_1912_04822_b200.pipeline import DatasetBatches
 
     N = cfg["batch"]
-    exs, _ = make_batch(cfg, rank, ws, n=max(pool, N))
+    xrng = np.random.default_rng(1000 * cfg["seed"] + 17 + rank)
+    exs = list(exs) + [synthetic.complex_example(xrng, vector=cfg["vector"])
+                       for _ in range(max(pool, N) - len(exs))]
     t0 = time.perf_counter()
     ds = DeviceDataset(exs, device=dev)
     build_s = time.perf_counter() - t0
@@ -595,7 +597,7 @@ def main():
     # dataset (DeviceDataset), each batch assembled on the device ----
     e2e_fresh = None
     if not args.no_e2e and not cfg.get("ligand_only"):
-        e2e_fresh = fresh_leg(args, cfg, gm, rank, ws, dev, stream, ev, barrier, out, tg)
+        e2e_fresh = fresh_leg(args, cfg, gm, rank, ws, dev, stream, ev, barrier, out, tg, exs)
 
     # the latency case (one small example per call): the same step captured as
     # CUDA graphs (GridMaker.capture_step), one transforms upload + one replay
